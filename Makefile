@@ -1,0 +1,29 @@
+# Builds the B200 sort library (sm_100a only) and the test oracles.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+           -Iinclude -Ipaper_1105_6040_b200/csrc --expt-relaxed-constexpr
+SRC := paper_1105_6040_b200/csrc
+LIB := paper_1105_6040_b200/lib
+OBJ := build/obj
+CU := abi radix_sort merge_path sample_sort gen_verify
+OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(CU)))
+HDRS := include/b200sort.h $(SRC)/b2s_internal.cuh
+
+all: $(LIB)/libb200sort.so
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(OBJ)/$*.ptxas.txt || (cat $(OBJ)/$*.ptxas.txt; exit 1)
+
+$(LIB)/libb200sort.so: $(OBJS)
+	@mkdir -p $(LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	bash oracle/build_ref.sh
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all oracle clean

@@ -1,0 +1,341 @@
+"""Benchmark: sorted keys/s on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N=1 workload (BASELINE.json configs[1], "cfg2"): 2^28 uint32 keys, the
+gen_data splitmix64 stream (seed 1) >> 32, i.e. uniform over the full 32-bit
+range, p=1 -- a pure local radix sort, 4 digit passes of 8 bits. One step =
+one b2s_sort of the 1 GiB key array, input resident in HBM (inputs are larger
+than L2, so no flush is needed between steps).
+
+N>1 (torchrun, one process per GPU, NCCL): the multi-GPU sample sort of
+configs[2] with 2^28 int32 keys per GPU (2^31 total at N=8; weak scaling):
+local sort, 64 regular samples per GPU, all-gather, splitters, bucket bounds,
+NCCL all-to-all, k-way merge of the received runs.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libsortbench_ref.so, parallel::scatter_merge_sort, merge, p = k =
+host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted keys/sec"
+UNIT = "keys/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks", suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref = the reference library compiled from source)
+
+def cpu_reference(sample_n: int, reps: int = 3):
+    """parallel::scatter_merge_sort (merge, wall mode, p = k = host threads) on
+    `sample_n` keys of the workload's distribution widened to int64 (the
+    reference's only Element type); run_benchmark's semantics: median of reps
+    of the world's wall seconds (P/src/bench.cpp:106-169)."""
+    import numpy as np
+
+    import oracle
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    z = oracle.gen_data(sample_n, 1).view(np.uint64)
+    data = (z >> np.uint64(32)).astype(np.int64)
+    if oracle.ref_available():
+        kind = "reference"
+        times = []
+        for _ in range(reps):
+            out, secs = oracle.ref_scatter_merge_sort(data, threads, "merge", cores=threads,
+                                                      wall=True)
+            times.append(secs)
+        t = sorted(times)[(len(times) - 1) // 2]
+    else:  # the C restatement, single thread
+        kind, threads = "port", 1
+        t0 = time.perf_counter()
+        out = oracle.scatter_merge_sort(data, 1)
+        t = time.perf_counter() - t0
+    if not (out[1:] >= out[:-1]).all():
+        raise RuntimeError("CPU baseline produced unsorted output")
+    return {"value": sample_n / t, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{sample_n} keys (cfg2 distribution widened to int64), "
+                      f"scatter_merge_sort merge p=k={threads}, median of {reps} wall-mode reps"}
+
+
+def run_reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return
+    sample_n = args.ref_sample
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        b = cpu_reference(sample_n, reps=1)
+        if i >= args.warmup:
+            vals.append(b["value"])
+        base = b
+    v = statistics.median(vals)
+    t_ms = sample_n / v * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (gen_data splitmix64 seed 1)",
+        "config": {"workload": "cfg2 sample on host CPU", "n": sample_n,
+                   "p": base["cores"], "algorithm": "merge"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
+                         "sample": base["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm, N = 1
+
+def run_single(args):
+    import numpy as np
+    import torch
+
+    from paper_1105_6040_b200.device import Context
+
+    hbm_peak, peak_kind = _peaks()
+    torch.cuda.set_device(0)
+    ctx = Context(0)
+    n = args.n
+    keys = ctx.gen_keys(n, 1, torch.uint32, shift=32)
+    out = torch.empty_like(keys)
+    torch.cuda.synchronize()
+
+    # correctness gate on the benchmarked data (untimed, like verify_output)
+    _, _, ms_in = ctx.check_sorted(keys)
+    ctx.sort(keys, out=out)
+    inv, _, ms_out = ctx.check_sorted(out)
+    if inv != 0 or ms_in != ms_out:
+        raise RuntimeError("bench: sorted output failed verification")
+
+    for _ in range(args.warmup):
+        ctx.sort(keys, out=out)
+    torch.cuda.synchronize()
+
+    # timed region: K sorts, CUDA events on the stream the kernels run on
+    stream = torch.cuda.current_stream()
+    clocks = Clocks(0)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        ctx.sort(keys, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    ms_step = total_ms / args.steps
+
+    # per-kernel durations (CUDA events around each launch inside the ABI)
+    ctx.enable_timing(True)
+    pass_ms, hist_ms, executed = [], [], 0
+    for _ in range(args.steps):
+        ctx.sort(keys, out=out)
+        t = ctx.timing()
+        pass_ms.extend(t.pass_ms)
+        hist_ms.append(t.hist_ms)
+        executed = t.passes_executed
+    ctx.enable_timing(False)
+    clk = clocks.stop()
+
+    # end to end through the C ABI with pinned HOST buffers (H2D + sort + D2H)
+    h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_in.copy_(keys.view(torch.int32).cpu())
+    h_out = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    hin_np = h_in.numpy().view(np.uint32)
+    hout_np = h_out.numpy().view(np.uint32)
+    e2e_steps = max(1, min(args.steps, 5))
+    ctx.sort(hin_np, out=hout_np)  # warm the staging buffers
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.sort(hin_np, out=hout_np)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if not (hout_np[1:] >= hout_np[:-1]).all():
+        raise RuntimeError("bench: e2e output unsorted")
+
+    avg_pass = statistics.mean(pass_ms)
+    alg_bytes = 2 * 4 * n  # read + write of every 4-byte key per pass
+    achieved = alg_bytes / (avg_pass * 1e-3) / 1e9
+    value = n / (ms_step * 1e-3)
+    cpu = cpu_reference(args.cpu_sample, reps=3) if not args.no_cpu else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (gen_data splitmix64 seed 1 >> 32, uniform 32-bit)",
+        "config": {"workload": "cfg2: 2^28 uint32 keys, p=1, 4 x 8-bit LSD passes",
+                   "n": n, "p": 1, "key_bytes": 4,
+                   "l2": "inputs (1 GiB) larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "onesweep_kernel (one digit pass)",
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": avg_pass},
+        "phases_ms": {"hist_plus_plan": statistics.mean(hist_ms),
+                      "pass_avg": avg_pass, "passes_executed": executed},
+        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+                "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_s * 1e3,
+                "path": "b2s_sort(B2S_HOST) from pinned host memory"},
+        "gpu_launches": args.steps * (3 + executed),
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+# ---------------------------------------------------------------------------
+# B200 arm, N > 1 (torchrun)
+
+def run_multi(args, rank: int, world: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1105_6040_b200.device import Context
+    from paper_1105_6040_b200.sample_sort import SampleSorter
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ctx = Context(local)
+    n_local = args.n_per_gpu
+    total = n_local * world
+    # shard r holds keys [r*n_local, (r+1)*n_local) of the cfg3 stream (int32 = z >> 33)
+    keys = ctx.gen_keys(n_local, 1, torch.int32, shift=33, first=rank * n_local)
+    sorter = SampleSorter(ctx, samples_per_rank=64)
+    out = sorter.sort(keys)
+    ok = sorter.verify(out)
+    if not ok:
+        raise RuntimeError(f"rank {rank}: sample sort verification failed")
+    for _ in range(args.warmup):
+        sorter.sort(keys)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        sorter.sort(keys)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    clk = clocks.stop()
+    ms_step = float(ms.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": total / (ms_step * 1e-3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "i32",
+            "data": "synthetic (gen_data splitmix64 seed 1 >> 33, int32 in [0, 2^31))",
+            "config": {"workload": "cfg3: sample sort, 2^28 int32 keys per GPU, 64 samples/GPU",
+                       "n_per_gpu": n_local, "parallelism": f"sample sort over {world} GPUs"},
+            "gpu_launches": None, "clocks": clk, "phases_ms": sorter.last_phase_ms,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 28)
+    ap.add_argument("--n-per-gpu", type=int, default=1 << 28)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--ref-sample", type=int, default=1 << 24)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        run_multi(args, rank, world)
+    else:
+        run_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/*
+ * b200sort.h -- C ABI of the B200-native partitioned sort.
+ *
+ * This is the drop-in boundary for the hot path of the reference
+ * (/root/reference/proj, "sortbench"): scatter N keys over p partitions, sort
+ * each partition, merge the sorted runs into one ascending array. The
+ * reference's C++ entry points keep their signatures in
+ * include/sortbench_b200/ and call down into these
+ * functions; nothing here uses C++ or torch types.
+ *
+ * Conventions
+ *   - Every function returns a b2s_status; on failure b2s_last_error() (a
+ *     thread-local string) says why. The reference throws instead
+ *     (P/include/sortbench/errors.hpp:10-46); the shims map EINVAL ->
+ *     ConfigError, EINTERNAL -> ProgrammingError, the rest -> runtime_error.
+ *   - Pointers are DEVICE pointers unless the call takes `flags` and
+ *     B2S_HOST is set, in which case they are host pointers (pinned memory
+ *     gives full PCIe bandwidth) and the call is synchronous.
+ *   - DEVICE calls are asynchronous on the context's stream (b2s_set_stream).
+ *   - A context is bound to one device and must be used by one host thread
+ *     at a time (the reference runs one rank per thread,
+ *     P/src/runtime.cpp:683-688: give each thread its own context).
+ *   - There is no CPU fallback: without a usable sm_100 device b2s_create
+ *     fails with B2S_ECUDA.
+ */
+#ifndef B200SORT_H
+#define B200SORT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum b2s_status {
+    B2S_OK = 0,
+    B2S_EINVAL = 1,    /* bad argument / configuration   -> ConfigError      */
+    B2S_ENOMEM = 2,    /* device or pinned allocation failed                 */
+    B2S_ECUDA = 3,     /* CUDA runtime / launch error                        */
+    B2S_EINTERNAL = 4  /* internal invariant violated    -> ProgrammingError */
+} b2s_status;
+
+/* Key types. The reference sorts int64 only (Element,
+ * P/include/sortbench/element.hpp:10); the GPU path also sorts the 32-bit and
+ * unsigned widths named by BASELINE.json. Signed keys order as signed. */
+typedef enum b2s_dtype { B2S_I32 = 0, B2S_U32 = 1, B2S_I64 = 2, B2S_U64 = 3 } b2s_dtype;
+
+#define B2S_DEVICE 0u
+#define B2S_HOST 1u
+
+typedef struct b2s_ctx b2s_ctx;
+
+/* Regular-sampling record used by the multi-GPU sample sort: `key` is the
+ * key's order-preserving unsigned image (sign bit flipped for signed types),
+ * `tag` = (rank << 40) | position-in-sorted-shard, so (key, tag) is a total
+ * order that equals (key, global index) for a stable local sort. A slot with
+ * key = tag = UINT64_MAX is empty. */
+typedef struct b2s_sample {
+    uint64_t key;
+    uint64_t tag;
+} b2s_sample;
+
+/* Device-side phase timings of the most recent sort/merge call on a context
+ * with timing enabled (CUDA events on the context's stream). */
+typedef struct b2s_timing {
+    float hist_ms;           /* upfront all-digit histogram + pass plan            */
+    float pass_ms[8];        /* onesweep digit pass per executed slot               */
+    int passes_executed;     /* digit passes that ran (constant digits are skipped) */
+    int passes_possible;     /* 4 for 32-bit keys, 8 for 64-bit keys                */
+    float copy_ms;           /* trailing copy (odd pass count in place), else 0     */
+    float merge_ms;          /* merge-path rounds (b2s_merge / partitioned sort)    */
+    int merge_rounds;
+    float total_ms;          /* first event to last event of the call               */
+} b2s_timing;
+
+/* ---- context ----------------------------------------------------------- */
+b2s_status b2s_create(int device, b2s_ctx** out);
+b2s_status b2s_destroy(b2s_ctx* ctx);
+/* `stream` is a cudaStream_t; NULL selects the context's own stream. */
+b2s_status b2s_set_stream(b2s_ctx* ctx, void* stream);
+b2s_status b2s_synchronize(b2s_ctx* ctx);
+b2s_status b2s_enable_timing(b2s_ctx* ctx, int on);
+b2s_status b2s_get_timing(b2s_ctx* ctx, b2s_timing* out);
+const char* b2s_last_error(void);
+const char* b2s_version(void);
+int b2s_device_count(void);
+
+/* ---- local sort ----------------------------------------------------------
+ * Replaces the per-rank comparison kernels behind KernelFn
+ * (P/include/sortbench/parallel_sort.hpp:69-72; kernels::merge_sort /
+ * quick_sort / bubble_sort, P/src/sort_core.cpp:23-144) with an LSD onesweep
+ * radix sort. keys_in -> keys_out (they may alias: in-place). vals_in/vals_out
+ * are an optional uint32 payload (both NULL or both non-NULL) permuted with
+ * the keys; the sort is stable, so equal keys keep their payload order. */
+b2s_status b2s_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* keys_in, void* keys_out,
+                    const uint32_t* vals_in, uint32_t* vals_out, uint64_t n, uint32_t flags);
+
+/* ---- k-way merge ---------------------------------------------------------
+ * Replaces the odd-even merge_split phases + rank-order gather of the root
+ * merge (P/src/parallel_sort.cpp:59-134,217-248): merges k sorted runs into
+ * `out`, stably, ties taken from the lower run index (kernels::merge_runs'
+ * rule, P/src/sort_core.cpp:46). `runs`, `run_vals` and `lens` are HOST
+ * arrays of k entries; the run pointers are device pointers (or host pointers
+ * with B2S_HOST). `out` must not overlap any run. */
+b2s_status b2s_merge(b2s_ctx* ctx, b2s_dtype dtype, const void* const* runs,
+                     const uint32_t* const* run_vals, const uint64_t* lens, int k, void* out,
+                     uint32_t* out_vals, uint32_t flags);
+
+/* ---- whole single-GPU path ----------------------------------------------
+ * parallel::scatter_merge_sort on one device (P/src/parallel_sort.cpp:166-254):
+ * split `in` into p contiguous partitions by plan_partition (:26-38), sort
+ * each partition, merge the p runs into `out` (may alias `in`). p >= 1. */
+b2s_status b2s_partitioned_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, void* out,
+                                const uint32_t* vals_in, uint32_t* vals_out, uint64_t n,
+                                int p, uint32_t flags);
+
+/* plan_partition (P/src/parallel_sort.cpp:26-38): the first n mod p
+ * partitions get one extra key. sizes has p slots (host). */
+b2s_status b2s_plan_partition(uint64_t n, int p, uint64_t* sizes);
+
+/* ---- odd-even merge-split (the reference's own exchange step) -----------
+ * merge_split_padded (P/src/parallel_sort.cpp:115-134) on the device: `mine`
+ * and `theirs` are sorted runs padded with virtual top sentinels to the same
+ * width; keeps the low (keep_high = 0) or high width elements. Writes the kept
+ * reals to out_reals and their count / the kept virtual count to the host
+ * integers. */
+b2s_status b2s_merge_split_padded(b2s_ctx* ctx, b2s_dtype dtype, const void* mine,
+                                  uint64_t n_mine, uint64_t mine_virtuals, const void* theirs,
+                                  uint64_t n_theirs, uint64_t theirs_virtuals, int keep_high,
+                                  void* out_reals, uint64_t* out_n_reals,
+                                  uint64_t* out_virtuals, uint32_t flags);
+
+/* ---- sample sort building blocks (one process per GPU) ------------------
+ * These replace Comm::scatter/gather and the p odd-even phases
+ * (P/src/runtime.cpp:509-568, P/src/parallel_sort.cpp:188-248) across GPUs:
+ *   local b2s_sort -> b2s_sample_regular -> all-gather samples ->
+ *   b2s_select_splitters -> b2s_bucket_bounds -> all-to-all -> b2s_merge.
+ * All pointers are device pointers. */
+b2s_status b2s_sample_regular(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_keys,
+                              uint64_t n, int rank, int samples, b2s_sample* out);
+b2s_status b2s_select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count,
+                                int nparts, b2s_sample* splitters);
+b2s_status b2s_bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_keys,
+                             uint64_t n, int rank, const b2s_sample* splitters, int nparts,
+                             uint64_t* bounds);
+
+/* ---- input generation and verification ----------------------------------
+ * b2s_gen_keys: key_i = (T)(z_{first+i} >> shift) where z is bench::gen_data's
+ * splitmix64 stream for `seed` (P/src/bench.cpp:57-71) -- bit-identical to the
+ * host generator. b2s_check_sorted: adjacent-inversion count, the golden
+ * fixtures' order-sensitive fingerprint (sum_i mix(w_i ^ mix(i+1)) over the
+ * int64/uint64 widening w) and an order-independent multiset hash
+ * (sum_i mix(w_i)), all returned to host integers (synchronous). */
+b2s_status b2s_gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n,
+                        uint64_t seed, int shift, void* out);
+b2s_status b2s_check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
+                            uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B200SORT_H */

@@ -1,0 +1,506 @@
+// abi.cu -- the extern "C" boundary (include/b200sort.h).
+//
+// Argument checking, context/scratch ownership, host<->device staging for
+// B2S_HOST calls, CUDA-event phase timing, and the thread-local error string.
+// Each entry point cites the reference interface it stands in for.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "b2s_internal.cuh"
+
+namespace b2s {
+
+namespace {
+thread_local std::string g_err;
+}
+
+b2s_status set_error(b2s_status st, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+void clear_error() { g_err.clear(); }
+
+b2s_status DevBuf::ensure(size_t want) {
+    if (want <= bytes && ptr != nullptr) return B2S_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t sz = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&ptr, sz);
+    if (e != cudaSuccess) {
+        ptr = nullptr;
+        cudaGetLastError();
+        return set_error(B2S_ENOMEM, "cudaMalloc(%zu) failed: %s", sz, cudaGetErrorString(e));
+    }
+    bytes = sz;
+    return B2S_OK;
+}
+
+void DevBuf::release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+}
+
+b2s_status HostBuf::ensure(size_t want) {
+    if (want <= bytes && ptr != nullptr) return B2S_OK;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t sz = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMallocHost(&ptr, sz);
+    if (e != cudaSuccess) {
+        ptr = nullptr;
+        cudaGetLastError();
+        return set_error(B2S_ENOMEM, "cudaMallocHost(%zu) failed: %s", sz, cudaGetErrorString(e));
+    }
+    bytes = sz;
+    return B2S_OK;
+}
+
+void HostBuf::release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+}
+
+int record(b2s_ctx* ctx) {
+    if (!ctx->timing || ctx->n_events >= 40) return -1;
+    const int i = ctx->n_events++;
+    if (cudaEventRecord(ctx->ev[i], ctx->stream) != cudaSuccess) return -1;
+    return i;
+}
+
+void timing_reset(b2s_ctx* ctx) {
+    ctx->n_events = 0;
+    ctx->ev_hist0 = ctx->ev_hist1 = ctx->ev_copy1 = -1;
+    ctx->ev_merge0 = ctx->ev_merge1 = -1;
+    for (int s = 0; s <= kMaxSlots; ++s) ctx->ev_pass[s] = -1;
+    ctx->have_sort = ctx->have_merge = false;
+    ctx->last_passes_possible = 0;
+    ctx->last_merge_rounds = 0;
+}
+
+}  // namespace b2s
+
+using namespace b2s;
+
+namespace {
+
+b2s_status check_ctx(b2s_ctx* ctx) {
+    if (ctx == nullptr) return set_error(B2S_EINVAL, "null context");
+    B2S_CUDA(cudaSetDevice(ctx->device));
+    clear_error();
+    return B2S_OK;
+}
+
+float elapsed(b2s_ctx* ctx, int a, int b) {
+    if (a < 0 || b < 0) return 0.f;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.f;
+    }
+    return ms;
+}
+
+// Stages host inputs into device scratch for a B2S_HOST call.
+b2s_status h2d(b2s_ctx* ctx, DevBuf& buf, const void* src, size_t bytes) {
+    B2S_TRY(buf.ensure(bytes));
+    if (bytes)
+        B2S_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return B2S_OK;
+}
+
+b2s_status d2h_sync(b2s_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes)
+        B2S_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    return B2S_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* b2s_last_error(void) { return g_err.c_str(); }
+
+const char* b2s_version(void) { return "b200sort 0.1 (sm_100a onesweep radix + merge path)"; }
+
+int b2s_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+b2s_status b2s_create(int device, b2s_ctx** out) {
+    if (out == nullptr) return set_error(B2S_EINVAL, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return set_error(B2S_ECUDA, "no CUDA device available (%s); there is no CPU fallback",
+                         e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+    }
+    if (device < 0 || device >= count)
+        return set_error(B2S_EINVAL, "device %d out of range [0, %d)", device, count);
+    B2S_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    B2S_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return set_error(B2S_ECUDA, "device %d is sm_%d%d; this library is built for sm_100a",
+                         device, prop.major, prop.minor);
+    b2s_ctx* ctx = new b2s_ctx();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return set_error(B2S_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+    ctx->stream = ctx->own_stream;
+    for (int i = 0; i < 40; ++i) cudaEventCreate(&ctx->ev[i]);
+    // the histogram buffer is self-cleaning after its first zeroing
+    b2s_status st = ctx->hist.ensure(kMaxSlots * 256 * sizeof(unsigned long long));
+    if (st == B2S_OK) {
+        e = cudaMemset(ctx->hist.ptr, 0, kMaxSlots * 256 * sizeof(unsigned long long));
+        if (e != cudaSuccess) st = set_error(B2S_ECUDA, "cudaMemset: %s", cudaGetErrorString(e));
+    }
+    if (st != B2S_OK) {
+        b2s_destroy(ctx);
+        return st;
+    }
+    timing_reset(ctx);
+    *out = ctx;
+    return B2S_OK;
+}
+
+b2s_status b2s_destroy(b2s_ctx* ctx) {
+    if (ctx == nullptr) return B2S_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->alt_keys, &ctx->alt_vals,  &ctx->seg_keys,  &ctx->seg_vals,
+                      &ctx->lookback, &ctx->hist,      &ctx->plan,      &ctx->parts,
+                      &ctx->misc,     &ctx->stage_in,  &ctx->stage_out, &ctx->stage_vin,
+                      &ctx->stage_vout};
+    for (DevBuf* b : bufs) b->release();
+    ctx->host_misc.release();
+    for (int i = 0; i < 40; ++i)
+        if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return B2S_OK;
+}
+
+b2s_status b2s_set_stream(b2s_ctx* ctx, void* stream) {
+    B2S_TRY(check_ctx(ctx));
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return B2S_OK;
+}
+
+b2s_status b2s_synchronize(b2s_ctx* ctx) {
+    B2S_TRY(check_ctx(ctx));
+    B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    return B2S_OK;
+}
+
+b2s_status b2s_enable_timing(b2s_ctx* ctx, int on) {
+    B2S_TRY(check_ctx(ctx));
+    ctx->timing = on != 0;
+    timing_reset(ctx);
+    return B2S_OK;
+}
+
+b2s_status b2s_get_timing(b2s_ctx* ctx, b2s_timing* out) {
+    B2S_TRY(check_ctx(ctx));
+    if (out == nullptr) return set_error(B2S_EINVAL, "null timing output");
+    *out = b2s_timing{};
+    if (!ctx->timing) return set_error(B2S_EINVAL, "timing is not enabled on this context");
+    B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->have_sort) {
+        out->hist_ms = elapsed(ctx, ctx->ev_hist0, ctx->ev_hist1);
+        out->passes_possible = ctx->last_passes_possible;
+        int executed = 0;
+        RadixPlan* plan = static_cast<RadixPlan*>(ctx->plan.ptr);
+        if (plan) {
+            int na = 0;
+            B2S_CUDA(cudaMemcpy(&na, &plan->num_active, sizeof(int), cudaMemcpyDeviceToHost));
+            executed = na;
+        }
+        out->passes_executed = executed;
+        for (int s = 0; s < executed && s < kMaxSlots; ++s)
+            out->pass_ms[s] = elapsed(ctx, ctx->ev_pass[s], ctx->ev_pass[s + 1]);
+        const int last = ctx->ev_pass[ctx->last_passes_possible];
+        out->copy_ms = elapsed(ctx, last >= 0 ? last : ctx->ev_hist1, ctx->ev_copy1);
+    }
+    if (ctx->have_merge) {
+        out->merge_ms = elapsed(ctx, ctx->ev_merge0, ctx->ev_merge1);
+        out->merge_rounds = ctx->last_merge_rounds;
+    }
+    if (ctx->n_events >= 2) out->total_ms = elapsed(ctx, 0, ctx->n_events - 1);
+    return B2S_OK;
+}
+
+b2s_status b2s_plan_partition(uint64_t n, int p, uint64_t* sizes) {
+    clear_error();
+    if (p < 1) return set_error(B2S_EINVAL, "partition needs at least one process");
+    if (sizes == nullptr) return set_error(B2S_EINVAL, "null sizes");
+    const uint64_t base = n / (uint64_t)p, extra = n % (uint64_t)p;
+    for (int r = 0; r < p; ++r) sizes[r] = base + ((uint64_t)r < extra ? 1 : 0);
+    return B2S_OK;
+}
+
+b2s_status b2s_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* keys_in, void* keys_out,
+                    const uint32_t* vals_in, uint32_t* vals_out, uint64_t n, uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if ((vals_in == nullptr) != (vals_out == nullptr))
+        return set_error(B2S_EINVAL, "vals_in and vals_out must both be set or both be NULL");
+    if (n > 0 && (keys_in == nullptr || keys_out == nullptr))
+        return set_error(B2S_EINVAL, "null key buffer with n = %llu", (unsigned long long)n);
+    if (n >= (1ull << 40)) return set_error(B2S_EINVAL, "n = %llu exceeds 2^40", (unsigned long long)n);
+    const size_t kb = (size_t)key_bytes(dtype) * n, vb = 4 * n;
+    timing_reset(ctx);
+    if (flags & B2S_HOST) {
+        B2S_TRY(h2d(ctx, ctx->stage_in, keys_in, kb));
+        if (vals_in) B2S_TRY(h2d(ctx, ctx->stage_vin, vals_in, vb));
+        void* dk = ctx->stage_in.ptr;
+        uint32_t* dv = vals_in ? static_cast<uint32_t*>(ctx->stage_vin.ptr) : nullptr;
+        B2S_TRY(radix_sort(ctx, dtype, dk, dk, dv, dv, n));
+        ctx->have_sort = true;
+        B2S_TRY(d2h_sync(ctx, keys_out, dk, kb));
+        if (vals_out) B2S_TRY(d2h_sync(ctx, vals_out, dv, vb));
+        return B2S_OK;
+    }
+    B2S_TRY(radix_sort(ctx, dtype, keys_in, keys_out, vals_in, vals_out, n));
+    ctx->have_sort = true;
+    return B2S_OK;
+}
+
+b2s_status b2s_merge(b2s_ctx* ctx, b2s_dtype dtype, const void* const* runs,
+                     const uint32_t* const* run_vals, const uint64_t* lens, int k, void* out,
+                     uint32_t* out_vals, uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (k < 0) return set_error(B2S_EINVAL, "negative run count");
+    if (k > 0 && (runs == nullptr || lens == nullptr))
+        return set_error(B2S_EINVAL, "null run arrays");
+    if ((run_vals == nullptr) != (out_vals == nullptr))
+        return set_error(B2S_EINVAL, "run_vals and out_vals must both be set or both be NULL");
+    const size_t ksz = (size_t)key_bytes(dtype);
+    uint64_t total = 0;
+    for (int i = 0; i < k; ++i) {
+        if (lens[i] > 0 && runs[i] == nullptr) return set_error(B2S_EINVAL, "run %d is NULL", i);
+        total += lens[i];
+    }
+    if (total > 0 && out == nullptr) return set_error(B2S_EINVAL, "null output");
+    timing_reset(ctx);
+    if (total == 0) return B2S_OK;
+    if (!(flags & B2S_HOST)) {
+        // out must not overlap a run (the merge rounds write it while reading)
+        const char* o0 = static_cast<const char*>(out);
+        const char* o1 = o0 + total * ksz;
+        for (int i = 0; i < k; ++i) {
+            const char* r0 = static_cast<const char*>(runs[i]);
+            const char* r1 = r0 + lens[i] * ksz;
+            if (lens[i] && r0 < o1 && o0 < r1)
+                return set_error(B2S_EINVAL, "output overlaps run %d", i);
+        }
+    }
+    B2S_TRY(ctx->alt_keys.ensure(total * ksz));
+    if (out_vals) B2S_TRY(ctx->alt_vals.ensure(total * 4));
+    if (flags & B2S_HOST) {
+        // stage all runs contiguously
+        B2S_TRY(ctx->stage_in.ensure(total * ksz));
+        B2S_TRY(ctx->stage_out.ensure(total * ksz));
+        if (out_vals) {
+            B2S_TRY(ctx->stage_vin.ensure(total * 4));
+            B2S_TRY(ctx->stage_vout.ensure(total * 4));
+        }
+        std::vector<const void*> dr(k);
+        std::vector<const uint32_t*> dv(k, nullptr);
+        uint64_t off = 0;
+        for (int i = 0; i < k; ++i) {
+            char* dst = static_cast<char*>(ctx->stage_in.ptr) + off * ksz;
+            if (lens[i])
+                B2S_CUDA(cudaMemcpyAsync(dst, runs[i], lens[i] * ksz, cudaMemcpyHostToDevice,
+                                         ctx->stream));
+            dr[i] = dst;
+            if (out_vals) {
+                uint32_t* vd = static_cast<uint32_t*>(ctx->stage_vin.ptr) + off;
+                if (lens[i])
+                    B2S_CUDA(cudaMemcpyAsync(vd, run_vals[i], lens[i] * 4,
+                                             cudaMemcpyHostToDevice, ctx->stream));
+                dv[i] = vd;
+            }
+            off += lens[i];
+        }
+        B2S_TRY(kway_merge(ctx, dtype, dr.data(), out_vals ? dv.data() : nullptr, lens, k,
+                           ctx->stage_out.ptr,
+                           out_vals ? static_cast<uint32_t*>(ctx->stage_vout.ptr) : nullptr,
+                           ctx->alt_keys.ptr, static_cast<uint32_t*>(ctx->alt_vals.ptr)));
+        ctx->have_merge = true;
+        B2S_TRY(d2h_sync(ctx, out, ctx->stage_out.ptr, total * ksz));
+        if (out_vals) B2S_TRY(d2h_sync(ctx, out_vals, ctx->stage_vout.ptr, total * 4));
+        return B2S_OK;
+    }
+    B2S_TRY(kway_merge(ctx, dtype, runs, run_vals, lens, k, out, out_vals, ctx->alt_keys.ptr,
+                       static_cast<uint32_t*>(ctx->alt_vals.ptr)));
+    ctx->have_merge = true;
+    return B2S_OK;
+}
+
+b2s_status b2s_partitioned_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, void* out,
+                                const uint32_t* vals_in, uint32_t* vals_out, uint64_t n, int p,
+                                uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (p < 1) return set_error(B2S_EINVAL, "partition needs at least one process");
+    if ((vals_in == nullptr) != (vals_out == nullptr))
+        return set_error(B2S_EINVAL, "vals_in and vals_out must both be set or both be NULL");
+    if (n > 0 && (in == nullptr || out == nullptr))
+        return set_error(B2S_EINVAL, "null key buffer with n = %llu", (unsigned long long)n);
+    const size_t ksz = (size_t)key_bytes(dtype);
+    timing_reset(ctx);
+    if (n == 0) return B2S_OK;
+    const void* din = in;
+    const uint32_t* dvin = vals_in;
+    void* dout = out;
+    uint32_t* dvout = vals_out;
+    if (flags & B2S_HOST) {
+        B2S_TRY(h2d(ctx, ctx->stage_in, in, n * ksz));
+        din = dout = ctx->stage_in.ptr;
+        if (vals_in) {
+            B2S_TRY(h2d(ctx, ctx->stage_vin, vals_in, n * 4));
+            dvin = dvout = static_cast<uint32_t*>(ctx->stage_vin.ptr);
+        }
+    }
+    if (p == 1) {  // a single partition is the plain local sort
+        B2S_TRY(radix_sort(ctx, dtype, din, dout, dvin, dvout, n));
+        ctx->have_sort = true;
+        if (flags & B2S_HOST) {
+            B2S_TRY(d2h_sync(ctx, out, dout, n * ksz));
+            if (vals_out) B2S_TRY(d2h_sync(ctx, vals_out, dvout, n * 4));
+        }
+        return B2S_OK;
+    }
+    // scatter (plan_partition) + local sort of each partition into seg_*
+    std::vector<uint64_t> sizes(p);
+    b2s_plan_partition(n, p, sizes.data());
+    B2S_TRY(ctx->seg_keys.ensure(n * ksz));
+    if (dvin) B2S_TRY(ctx->seg_vals.ensure(n * 4));
+    std::vector<const void*> runs;
+    std::vector<const uint32_t*> vruns;
+    std::vector<uint64_t> lens;
+    uint64_t off = 0;
+    for (int r = 0; r < p; ++r) {
+        const char* src = static_cast<const char*>(din) + off * ksz;
+        char* dst = static_cast<char*>(ctx->seg_keys.ptr) + off * ksz;
+        const uint32_t* vs = dvin ? dvin + off : nullptr;
+        uint32_t* vd = dvin ? static_cast<uint32_t*>(ctx->seg_vals.ptr) + off : nullptr;
+        if (sizes[r]) B2S_TRY(radix_sort(ctx, dtype, src, dst, vs, vd, sizes[r]));
+        runs.push_back(dst);
+        vruns.push_back(vd);
+        lens.push_back(sizes[r]);
+        off += sizes[r];
+    }
+    ctx->have_sort = p == 1;
+    // root merge of the p sorted runs
+    B2S_TRY(ctx->alt_keys.ensure(n * ksz));
+    if (dvin) B2S_TRY(ctx->alt_vals.ensure(n * 4));
+    B2S_TRY(kway_merge(ctx, dtype, runs.data(), dvin ? vruns.data() : nullptr, lens.data(), p,
+                       dout, dvout, ctx->alt_keys.ptr, static_cast<uint32_t*>(ctx->alt_vals.ptr)));
+    ctx->have_merge = true;
+    if (flags & B2S_HOST) {
+        B2S_TRY(d2h_sync(ctx, out, dout, n * ksz));
+        if (vals_out) B2S_TRY(d2h_sync(ctx, vals_out, dvout, n * 4));
+    }
+    return B2S_OK;
+}
+
+b2s_status b2s_merge_split_padded(b2s_ctx* ctx, b2s_dtype dtype, const void* mine,
+                                  uint64_t n_mine, uint64_t mine_virtuals, const void* theirs,
+                                  uint64_t n_theirs, uint64_t theirs_virtuals, int keep_high,
+                                  void* out_reals, uint64_t* out_n_reals, uint64_t* out_virtuals,
+                                  uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (out_n_reals == nullptr || out_virtuals == nullptr)
+        return set_error(B2S_EINVAL, "null count outputs");
+    // like the reference, the kept width is mine's; theirs' width is not checked
+    const size_t ksz = (size_t)key_bytes(dtype);
+    timing_reset(ctx);
+    if (flags & B2S_HOST) {
+        B2S_TRY(h2d(ctx, ctx->stage_in, mine, n_mine * ksz));
+        B2S_TRY(h2d(ctx, ctx->stage_vin, theirs, n_theirs * ksz));
+        B2S_TRY(ctx->stage_out.ensure((n_mine + mine_virtuals) * ksz + 16));
+        B2S_TRY(merge_split_padded(ctx, dtype, ctx->stage_in.ptr, n_mine, mine_virtuals,
+                                   ctx->stage_vin.ptr, n_theirs, theirs_virtuals, keep_high,
+                                   ctx->stage_out.ptr, out_n_reals, out_virtuals));
+        return d2h_sync(ctx, out_reals, ctx->stage_out.ptr, *out_n_reals * ksz);
+    }
+    return merge_split_padded(ctx, dtype, mine, n_mine, mine_virtuals, theirs, n_theirs,
+                              theirs_virtuals, keep_high, out_reals, out_n_reals, out_virtuals);
+}
+
+b2s_status b2s_sample_regular(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_keys, uint64_t n,
+                              int rank, int samples, b2s_sample* out) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (samples < 1 || out == nullptr) return set_error(B2S_EINVAL, "need >= 1 sample slot");
+    if (rank < 0 || rank >= (1 << 23)) return set_error(B2S_EINVAL, "rank %d out of range", rank);
+    if (n >= (1ull << 40)) return set_error(B2S_EINVAL, "shard too large for sample tags");
+    return sample_regular(ctx, dtype, sorted_keys, n, rank, samples, out);
+}
+
+b2s_status b2s_select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count, int nparts,
+                                b2s_sample* splitters) {
+    B2S_TRY(check_ctx(ctx));
+    if (count < 0 || nparts < 1) return set_error(B2S_EINVAL, "bad sample/partition counts");
+    if (nparts > 1 && (samples == nullptr || splitters == nullptr))
+        return set_error(B2S_EINVAL, "null sample buffers");
+    return select_splitters(ctx, samples, count, nparts, splitters);
+}
+
+b2s_status b2s_bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_keys, uint64_t n,
+                             int rank, const b2s_sample* splitters, int nparts, uint64_t* bounds) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (nparts < 1 || bounds == nullptr) return set_error(B2S_EINVAL, "bad bounds arguments");
+    if (nparts > 1 && splitters == nullptr) return set_error(B2S_EINVAL, "null splitters");
+    return bucket_bounds(ctx, dtype, sorted_keys, n, rank, splitters, nparts, bounds);
+}
+
+b2s_status b2s_gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
+                        int shift, void* out) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (shift < 0 || shift > 63) return set_error(B2S_EINVAL, "shift %d out of range", shift);
+    if (n > 0 && out == nullptr) return set_error(B2S_EINVAL, "null output");
+    return gen_keys(ctx, dtype, first, n, seed, shift, out);
+}
+
+b2s_status b2s_check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
+                            uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (n > 0 && keys == nullptr) return set_error(B2S_EINVAL, "null keys");
+    return check_sorted(ctx, dtype, keys, n, inversions, fingerprint, multiset);
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// b2s_internal.cuh -- shared definitions of the B200 sort kernels and host side.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "b200sort.h"
+
+namespace b2s {
+
+// ---------------------------------------------------------------------------
+// error plumbing (thread-local message, status codes of b200sort.h)
+
+b2s_status set_error(b2s_status st, const char* fmt, ...);
+void clear_error();
+
+#define B2S_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return ::b2s::set_error(e_ == cudaErrorMemoryAllocation ? B2S_ENOMEM        \
+                                                                   : B2S_ECUDA,         \
+                                    "%s:%d %s -> %s", __FILE__, __LINE__, #call,         \
+                                    cudaGetErrorString(e_));                             \
+    } while (0)
+
+#define B2S_LAUNCHED() B2S_CUDA(cudaGetLastError())
+
+#define B2S_TRY(expr)                                \
+    do {                                             \
+        b2s_status s_ = (expr);                      \
+        if (s_ != B2S_OK) return s_;                 \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device scratch owned by a context, grown on demand, never shrunk
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    b2s_status ensure(size_t want);
+    void release();
+};
+
+struct HostBuf {  // pinned
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    b2s_status ensure(size_t want);
+    void release();
+};
+
+enum { kMaxSlots = 8 };
+
+// Per-call radix sort plan, written on the device by radix_plan_kernel from the
+// upfront histogram so that constant-digit passes are skipped without a host
+// round trip. Slot s runs digit position digit[s]; slots >= num_active exit.
+struct RadixPlan {
+    int num_active;
+    int do_copy;
+    int digit[kMaxSlots];
+    uint32_t dxor[kMaxSlots];  // 0x80 on the top digit of signed keys
+    const void* ksrc[kMaxSlots];
+    void* kdst[kMaxSlots];
+    const uint32_t* vsrc[kMaxSlots];
+    uint32_t* vdst[kMaxSlots];
+    const void* copy_ksrc;
+    void* copy_kdst;
+    const uint32_t* copy_vsrc;
+    uint32_t* copy_vdst;
+    unsigned int tile_counter[kMaxSlots];
+    unsigned long long digit_offset[kMaxSlots][256];
+};
+
+struct TimingEvents {
+    cudaEvent_t ev[32];
+    int used = 0;
+};
+
+}  // namespace b2s
+
+struct b2s_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+
+    // radix sort scratch
+    b2s::DevBuf alt_keys, alt_vals;      // ping-pong partner / merge temp
+    b2s::DevBuf seg_keys, seg_vals;      // partitioned sort: sorted segments
+    b2s::DevBuf lookback;                // 2 regions x tiles x 256 words
+    b2s::DevBuf hist;                    // 8 x 256 u64 (self-cleaning)
+    b2s::DevBuf plan;                    // RadixPlan
+    b2s::DevBuf parts;                   // merge-path partitions
+    b2s::DevBuf misc;                    // small reductions
+    b2s::HostBuf host_misc;              // pinned small results
+    // B2S_HOST staging
+    b2s::DevBuf stage_in, stage_out, stage_vin, stage_vout;
+
+    bool timing = false;
+    cudaEvent_t ev[40] = {};
+    int n_events = 0;
+    b2s_timing last{};
+    // event indices of the last call (-1 when absent)
+    int ev_hist0 = -1, ev_hist1 = -1, ev_pass[b2s::kMaxSlots + 1] = {}, ev_copy1 = -1;
+    int ev_merge0 = -1, ev_merge1 = -1;
+    int last_passes_possible = 0;
+    int last_merge_rounds = 0;
+    bool have_sort = false, have_merge = false;
+};
+
+namespace b2s {
+
+inline int key_bytes(b2s_dtype t) { return (t == B2S_I32 || t == B2S_U32) ? 4 : 8; }
+inline bool key_signed(b2s_dtype t) { return t == B2S_I32 || t == B2S_I64; }
+inline bool dtype_ok(int t) { return t >= B2S_I32 && t <= B2S_U64; }
+
+// timing helpers (no-ops unless ctx->timing)
+int record(b2s_ctx* ctx);
+void timing_reset(b2s_ctx* ctx);
+
+// device entry points implemented in the .cu files (all async on ctx->stream)
+b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout,
+                      const uint32_t* vin, uint32_t* vout, uint64_t n);
+b2s_status kway_merge(b2s_ctx* ctx, b2s_dtype dtype, const void* const* runs,
+                      const uint32_t* const* vals, const uint64_t* lens, int k, void* out,
+                      uint32_t* vout, void* tmp, uint32_t* vtmp);
+b2s_status merge_split_padded(b2s_ctx* ctx, b2s_dtype dtype, const void* mine, uint64_t nm,
+                              uint64_t mv, const void* theirs, uint64_t nt, uint64_t tv,
+                              int keep_high, void* out, uint64_t* out_n, uint64_t* out_v);
+b2s_status sample_regular(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
+                          int rank, int s, b2s_sample* out);
+b2s_status select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count, int nparts,
+                            b2s_sample* splitters);
+b2s_status bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n, int rank,
+                         const b2s_sample* splitters, int nparts, uint64_t* bounds);
+b2s_status gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
+                    int shift, void* out);
+b2s_status check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
+                        uint64_t* inv, uint64_t* fp, uint64_t* ms);
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+}  // namespace b2s

@@ -1,0 +1,291 @@
+// merge_path.cu -- stable merge-path merges for sm_100a.
+//
+// Replaces the root merge of the reference: the p odd-even merge_split phases
+// and the rank-order gather (P/src/parallel_sort.cpp:59-134,217-248), whose
+// result is the ascending concatenation of all blocks. kernels::merge_runs'
+// tie rule (P/src/sort_core.cpp:46: ties take run_a) is kept everywhere, so a
+// merge of runs 0..k-1 is stable with ties to the lower run index.
+//
+// 2-way merge of A and B into one output:
+//   merge_partition_kernel  one thread per output tile boundary: merge-path
+//                           binary search along the cross diagonal (log2 n
+//                           probes, all boundaries in parallel).
+//   merge_tile_kernel       one CTA per output tile: stage its A and B slices
+//                           in shared memory with coalesced loads, each thread
+//                           finds its own diagonal in shared memory and merges
+//                           ITEMS outputs, results are restaged and written
+//                           back with coalesced stores.
+// k-way merge: ceil(log2 k) rounds of pairwise merges, ping-ponging between
+// the output and a scratch buffer so the last round lands in the output.
+// merge_split_padded: one merge-path tile pass restricted to the kept half.
+#include <algorithm>
+
+#include "b2s_internal.cuh"
+
+namespace b2s {
+namespace {
+
+// Number of A elements among the first `diag` outputs of merge(A, B) with
+// ties taken from A first (a[i] <= b[j] -> a[i] goes first).
+template <typename T>
+__device__ __forceinline__ uint64_t merge_path(const T* a, uint64_t na, const T* b, uint64_t nb,
+                                               uint64_t diag) {
+    uint64_t lo = diag > nb ? diag - nb : 0;
+    uint64_t hi = diag < na ? diag : na;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (!(b[diag - 1 - mid] < a[mid])) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t merge_path_smem(const T* a, uint32_t na, const T* b,
+                                                    uint32_t nb, uint32_t diag) {
+    uint32_t lo = diag > nb ? diag - nb : 0;
+    uint32_t hi = diag < na ? diag : na;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (!(b[diag - 1 - mid] < a[mid])) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+constexpr int kMergeThreads = 256;
+template <typename T>
+struct MergeItems {
+    static constexpr int value = sizeof(T) == 4 ? 15 : 11;  // odd: conflict-free restaging
+};
+
+// Merges output positions [out_lo, out_hi) of merge(A, B) into out[0 ..).
+// Used both for full merges (out_lo = 0) and for merge_split's kept half.
+template <typename T, bool VALS>
+__global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
+    const T* __restrict__ a, const uint32_t* __restrict__ va, uint64_t na,
+    const T* __restrict__ b, const uint32_t* __restrict__ vb, uint64_t nb,
+    const uint64_t* __restrict__ parts, uint64_t out_lo, uint64_t out_hi, T* __restrict__ out,
+    uint32_t* __restrict__ vout) {
+    constexpr int ITEMS = MergeItems<T>::value;
+    constexpr int TILE = kMergeThreads * ITEMS;
+    __shared__ T s_k[TILE];
+    __shared__ uint32_t s_v[VALS ? TILE : 1];
+
+    const uint64_t t = blockIdx.x;
+    const uint64_t d0 = out_lo + t * TILE;
+    const uint64_t d1 = std::min<uint64_t>(d0 + TILE, out_hi);
+    const uint64_t a0 = parts[t], a1 = parts[t + 1];
+    const uint64_t b0 = d0 - a0, b1 = d1 - a1;
+    const uint32_t la = (uint32_t)(a1 - a0), lb = (uint32_t)(b1 - b0);
+    const uint32_t cnt = la + lb;
+
+    for (uint32_t i = threadIdx.x; i < la; i += kMergeThreads) {
+        s_k[i] = a[a0 + i];
+        if constexpr (VALS) s_v[i] = va[a0 + i];
+    }
+    for (uint32_t i = threadIdx.x; i < lb; i += kMergeThreads) {
+        s_k[la + i] = b[b0 + i];
+        if constexpr (VALS) s_v[la + i] = vb[b0 + i];
+    }
+    __syncthreads();
+
+    const uint32_t diag = std::min<uint32_t>(threadIdx.x * ITEMS, cnt);
+    uint32_t ai = merge_path_smem(s_k, la, s_k + la, lb, diag);
+    uint32_t bi = diag - ai;
+    T rk[ITEMS];
+    uint32_t rv[VALS ? ITEMS : 1];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        if (diag + j < cnt) {
+            const bool take_a = bi >= lb || (ai < la && !(s_k[la + bi] < s_k[ai]));
+            const uint32_t src = take_a ? ai++ : la + bi++;
+            rk[j] = s_k[src];
+            if constexpr (VALS) rv[j] = s_v[src];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        if (diag + j < cnt) {
+            s_k[threadIdx.x * ITEMS + j] = rk[j];
+            if constexpr (VALS) s_v[threadIdx.x * ITEMS + j] = rv[j];
+        }
+    }
+    __syncthreads();
+    const uint64_t o = d0 - out_lo;
+    for (uint32_t i = threadIdx.x; i < cnt; i += kMergeThreads) {
+        out[o + i] = s_k[i];
+        if constexpr (VALS) vout[o + i] = s_v[i];
+    }
+}
+
+template <typename T>
+__global__ void copy_kernel(const T* __restrict__ s, T* __restrict__ d, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        d[i] = s[i];
+}
+
+template <typename T>
+b2s_status copy_async(b2s_ctx* ctx, const T* s, T* d, uint64_t n) {
+    if (n == 0 || s == d) return B2S_OK;
+    B2S_CUDA(cudaMemcpyAsync(d, s, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+    return B2S_OK;
+}
+
+template <typename T>
+__global__ void merge_partition_window_kernel(const T* __restrict__ a, uint64_t na,
+                                              const T* __restrict__ b, uint64_t nb, uint64_t lo,
+                                              uint64_t hi, uint64_t tile, uint64_t nparts,
+                                              uint64_t* __restrict__ parts) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= nparts) return;
+    const uint64_t diag = std::min<uint64_t>(lo + i * tile, hi);
+    parts[i] = merge_path(a, na, b, nb, diag);
+}
+
+// output positions [lo, hi) of merge(a, b) -> out[0, hi-lo)
+template <typename T>
+b2s_status merge2_window(b2s_ctx* ctx, const T* a, const uint32_t* va, uint64_t na, const T* b,
+                         const uint32_t* vb, uint64_t nb, uint64_t lo, uint64_t hi, T* out,
+                         uint32_t* vout) {
+    constexpr int TILE = kMergeThreads * MergeItems<T>::value;
+    if (hi <= lo) return B2S_OK;
+    const uint64_t ntiles = (hi - lo + TILE - 1) / TILE;
+    const uint64_t np = ntiles + 1;
+    B2S_TRY(ctx->parts.ensure(np * sizeof(uint64_t)));
+    uint64_t* parts = static_cast<uint64_t*>(ctx->parts.ptr);
+    merge_partition_window_kernel<T><<<(unsigned)((np + 255) / 256), 256, 0, ctx->stream>>>(
+        a, na, b, nb, lo, hi, TILE, np, parts);
+    B2S_LAUNCHED();
+    if (va != nullptr)
+        merge_tile_kernel<T, true><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(
+            a, va, na, b, vb, nb, parts, lo, hi, out, vout);
+    else
+        merge_tile_kernel<T, false><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(
+            a, va, na, b, vb, nb, parts, lo, hi, out, vout);
+    B2S_LAUNCHED();
+    return B2S_OK;
+}
+
+struct Run {
+    const void* k;
+    const uint32_t* v;
+    uint64_t n;
+};
+
+template <typename T>
+b2s_status kway_t(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* vals,
+                  const uint64_t* lens, int k, void* out, uint32_t* vout, void* tmp,
+                  uint32_t* vtmp) {
+    const bool with_vals = vout != nullptr;
+    std::vector<Run> cur;
+    uint64_t total = 0;
+    for (int i = 0; i < k; ++i) {
+        cur.push_back({runs[i], with_vals ? vals[i] : nullptr, lens[i]});
+        total += lens[i];
+    }
+    int rounds = 0;
+    while ((1 << rounds) < k) ++rounds;
+    ctx->last_merge_rounds = rounds;
+    ctx->ev_merge0 = record(ctx);
+    if (k == 1) {
+        B2S_TRY(copy_async<T>(ctx, static_cast<const T*>(cur[0].k), static_cast<T*>(out), total));
+        if (with_vals) B2S_TRY(copy_async<uint32_t>(ctx, cur[0].v, vout, total));
+    }
+    for (int r = 0; r < rounds; ++r) {
+        const bool to_out = ((rounds - 1 - r) % 2) == 0;
+        T* dst = static_cast<T*>(to_out ? out : tmp);
+        uint32_t* vdst = with_vals ? (to_out ? vout : vtmp) : nullptr;
+        std::vector<Run> nxt;
+        uint64_t off = 0;
+        for (size_t i = 0; i < cur.size(); i += 2) {
+            if (i + 1 < cur.size()) {
+                const Run& A = cur[i];
+                const Run& B = cur[i + 1];
+                B2S_TRY(merge2_window<T>(ctx, static_cast<const T*>(A.k), A.v, A.n,
+                                         static_cast<const T*>(B.k), B.v, B.n, 0, A.n + B.n,
+                                         dst + off, vdst ? vdst + off : nullptr));
+                nxt.push_back({dst + off, vdst ? vdst + off : nullptr, A.n + B.n});
+                off += A.n + B.n;
+            } else {
+                // odd run out: move it into this round's buffer so no later round
+                // reads a buffer it is writing
+                const Run& A = cur[i];
+                B2S_TRY(copy_async<T>(ctx, static_cast<const T*>(A.k), dst + off, A.n));
+                if (vdst) B2S_TRY(copy_async<uint32_t>(ctx, A.v, vdst + off, A.n));
+                nxt.push_back({dst + off, vdst ? vdst + off : nullptr, A.n});
+                off += A.n;
+            }
+        }
+        cur.swap(nxt);
+    }
+    ctx->ev_merge1 = record(ctx);
+    return B2S_OK;
+}
+
+template <typename T>
+b2s_status merge_split_t(b2s_ctx* ctx, const void* mine, uint64_t nm, uint64_t mv,
+                         const void* theirs, uint64_t nt, uint64_t tv, int keep_high, void* out,
+                         uint64_t* out_n, uint64_t* out_v) {
+    // merge_split_padded, P/src/parallel_sort.cpp:115-134. Low side: the
+    // lowest min(width, reals) of merge(mine, theirs) with ties to mine
+    // (merge_take_low :74). High side: the highest `width - virtuals`, filled
+    // from the back taking theirs on ties (merge_take_high :97) -- the same
+    // sequence as the top of merge(mine, theirs) with ties to mine.
+    const uint64_t width = nm + mv;
+    const uint64_t reals = nm + nt;
+    if (!keep_high) {
+        const uint64_t take = std::min(width, reals);
+        *out_n = take;
+        *out_v = width - take;
+        return merge2_window<T>(ctx, static_cast<const T*>(mine), nullptr, nm,
+                                static_cast<const T*>(theirs), nullptr, nt, 0, take,
+                                static_cast<T*>(out), nullptr);
+    }
+    const uint64_t virt = std::min(width, mv + tv);
+    const uint64_t take = width - virt;
+    *out_n = take;
+    *out_v = virt;
+    return merge2_window<T>(ctx, static_cast<const T*>(mine), nullptr, nm,
+                            static_cast<const T*>(theirs), nullptr, nt, reals - take, reals,
+                            static_cast<T*>(out), nullptr);
+}
+
+}  // namespace
+
+b2s_status kway_merge(b2s_ctx* ctx, b2s_dtype dtype, const void* const* runs,
+                      const uint32_t* const* vals, const uint64_t* lens, int k, void* out,
+                      uint32_t* vout, void* tmp, uint32_t* vtmp) {
+    switch (dtype) {
+        case B2S_I32: return kway_t<int32_t>(ctx, runs, vals, lens, k, out, vout, tmp, vtmp);
+        case B2S_U32: return kway_t<uint32_t>(ctx, runs, vals, lens, k, out, vout, tmp, vtmp);
+        case B2S_I64: return kway_t<int64_t>(ctx, runs, vals, lens, k, out, vout, tmp, vtmp);
+        case B2S_U64:
+            return kway_t<unsigned long long>(ctx, runs, vals, lens, k, out, vout, tmp, vtmp);
+    }
+    return set_error(B2S_EINVAL, "bad dtype");
+}
+
+b2s_status merge_split_padded(b2s_ctx* ctx, b2s_dtype dtype, const void* mine, uint64_t nm,
+                              uint64_t mv, const void* theirs, uint64_t nt, uint64_t tv,
+                              int keep_high, void* out, uint64_t* out_n, uint64_t* out_v) {
+    switch (dtype) {
+        case B2S_I32:
+            return merge_split_t<int32_t>(ctx, mine, nm, mv, theirs, nt, tv, keep_high, out,
+                                          out_n, out_v);
+        case B2S_U32:
+            return merge_split_t<uint32_t>(ctx, mine, nm, mv, theirs, nt, tv, keep_high, out,
+                                           out_n, out_v);
+        case B2S_I64:
+            return merge_split_t<int64_t>(ctx, mine, nm, mv, theirs, nt, tv, keep_high, out,
+                                          out_n, out_v);
+        case B2S_U64:
+            return merge_split_t<unsigned long long>(ctx, mine, nm, mv, theirs, nt, tv,
+                                                     keep_high, out, out_n, out_v);
+    }
+    return set_error(B2S_EINVAL, "bad dtype");
+}
+
+}  // namespace b2s

@@ -1,0 +1,290 @@
+"""Python handle on the C ABI: a per-device context that sorts torch CUDA
+tensors (device pointers, asynchronous on torch's current stream) or numpy
+arrays (host pointers, B2S_HOST: copies inside the call, synchronous).
+
+PyTorch is plumbing here (device memory, streams); every compute step is a
+kernel in libb200sort.so.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import B2S_DEVICE, B2S_HOST, check, lib
+
+try:  # torch is optional for host-only use
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+_NP_DTYPES = {np.dtype(np.int32): _lib.B2S_I32, np.dtype(np.uint32): _lib.B2S_U32,
+              np.dtype(np.int64): _lib.B2S_I64, np.dtype(np.uint64): _lib.B2S_U64}
+
+
+def _torch_dtypes():
+    return {torch.int32: _lib.B2S_I32, torch.uint32: _lib.B2S_U32,
+            torch.int64: _lib.B2S_I64, torch.uint64: _lib.B2S_U64}
+
+
+def dtype_code(x) -> int:
+    if isinstance(x, np.ndarray):
+        try:
+            return _NP_DTYPES[x.dtype]
+        except KeyError:
+            raise TypeError(f"unsupported key dtype {x.dtype}") from None
+    try:
+        return _torch_dtypes()[x.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported key dtype {x.dtype}") from None
+
+
+def _is_host(x) -> bool:
+    return isinstance(x, np.ndarray)
+
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data if x.size else None
+    return x.data_ptr() if x.numel() else None
+
+
+def _check_1d(x, name):
+    if isinstance(x, np.ndarray):
+        if x.ndim != 1 or not x.flags.c_contiguous:
+            raise ValueError(f"{name} must be a contiguous 1-D array")
+    elif x is not None:
+        if x.dim() != 1 or not x.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 1-D tensor")
+        if not x.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (or pass a numpy array)")
+
+
+@dataclass
+class Timing:
+    hist_ms: float
+    pass_ms: list
+    passes_executed: int
+    passes_possible: int
+    copy_ms: float
+    merge_ms: float
+    merge_rounds: int
+    total_ms: float
+
+
+class Context:
+    """One b2s_ctx: bound to one CUDA device, used by one thread at a time."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = ctypes.c_void_p()
+        check(lib().b2s_create(device, ctypes.byref(h)))
+        self._h = h
+
+    # -- lifetime -----------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().b2s_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _bind_stream(self, stream=None) -> None:
+        if stream is None and torch is not None and torch.cuda.is_available():
+            stream = torch.cuda.current_stream(self.device)
+        s = None
+        if stream is not None:
+            s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        check(lib().b2s_set_stream(self._h, s))
+
+    def synchronize(self) -> None:
+        check(lib().b2s_synchronize(self._h))
+
+    def enable_timing(self, on: bool = True) -> None:
+        check(lib().b2s_enable_timing(self._h, int(on)))
+
+    def timing(self) -> Timing:
+        t = _lib.b2s_timing()
+        check(lib().b2s_get_timing(self._h, ctypes.byref(t)))
+        return Timing(t.hist_ms, list(t.pass_ms)[: t.passes_executed], t.passes_executed,
+                      t.passes_possible, t.copy_ms, t.merge_ms, t.merge_rounds, t.total_ms)
+
+    # -- local sort -----------------------------------------------------------
+    def sort(self, keys, out=None, vals=None, vals_out=None, stream=None):
+        """Sorts `keys` ascending (stable; `vals` is a uint32 payload permuted
+        with the keys). Returns (out, vals_out); out may be `keys` (in place)."""
+        _check_1d(keys, "keys")
+        host = _is_host(keys)
+        if out is None:
+            out = np.empty_like(keys) if host else torch.empty_like(keys)
+        if vals is not None and vals_out is None:
+            vals_out = np.empty_like(vals) if host else torch.empty_like(vals)
+        self._validate_pair(keys, out, vals, vals_out)
+        if not host:
+            self._bind_stream(stream)
+        check(lib().b2s_sort(self._h, dtype_code(keys), _ptr(keys), _ptr(out), _ptr(vals),
+                             _ptr(vals_out), _numel(keys), B2S_HOST if host else B2S_DEVICE))
+        return out, vals_out
+
+    def partitioned_sort(self, keys, p: int, out=None, vals=None, vals_out=None, stream=None):
+        """scatter / local sort / merge on this device with p partitions."""
+        _check_1d(keys, "keys")
+        host = _is_host(keys)
+        if out is None:
+            out = np.empty_like(keys) if host else torch.empty_like(keys)
+        if vals is not None and vals_out is None:
+            vals_out = np.empty_like(vals) if host else torch.empty_like(vals)
+        self._validate_pair(keys, out, vals, vals_out)
+        if not host:
+            self._bind_stream(stream)
+        check(lib().b2s_partitioned_sort(self._h, dtype_code(keys), _ptr(keys), _ptr(out),
+                                         _ptr(vals), _ptr(vals_out), _numel(keys), int(p),
+                                         B2S_HOST if host else B2S_DEVICE))
+        return out, vals_out
+
+    def merge(self, runs, vals=None, out=None, vals_out=None, stream=None):
+        """Stable k-way merge of sorted runs (ties to the lower run index)."""
+        if len(runs) == 0:
+            raise ValueError("merge needs at least one run")
+        for r in runs:
+            _check_1d(r, "run")
+        host = _is_host(runs[0])
+        total = sum(_numel(r) for r in runs)
+        code = dtype_code(runs[0])
+        for r in runs:
+            if dtype_code(r) != code or _is_host(r) != host:
+                raise TypeError("all runs must share dtype and memory space")
+        if out is None:
+            out = (np.empty(total, dtype=runs[0].dtype) if host
+                   else torch.empty(total, dtype=runs[0].dtype, device=runs[0].device))
+        if vals is not None and vals_out is None:
+            vals_out = (np.empty(total, dtype=np.uint32) if host
+                        else torch.empty(total, dtype=vals[0].dtype, device=vals[0].device))
+        k = len(runs)
+        rp = (ctypes.c_void_p * k)(*[_ptr(r) for r in runs])
+        ln = (ctypes.c_uint64 * k)(*[_numel(r) for r in runs])
+        vp = (ctypes.c_void_p * k)(*[_ptr(v) for v in vals]) if vals is not None else None
+        if not host:
+            self._bind_stream(stream)
+        check(lib().b2s_merge(self._h, code, rp, vp, ln, k, _ptr(out), _ptr(vals_out),
+                              B2S_HOST if host else B2S_DEVICE))
+        return out, vals_out
+
+    def merge_split_padded(self, mine, mine_virtuals: int, theirs, theirs_virtuals: int,
+                           keep_high: bool, stream=None):
+        """The reference's padded merge-split on the device; returns (reals, virtuals)."""
+        host = _is_host(mine)
+        width = _numel(mine) + mine_virtuals
+        out = (np.empty(max(width, 1), dtype=mine.dtype) if host
+               else torch.empty(max(width, 1), dtype=mine.dtype, device=mine.device))
+        nr, nv = ctypes.c_uint64(), ctypes.c_uint64()
+        if not host:
+            self._bind_stream(stream)
+        check(lib().b2s_merge_split_padded(
+            self._h, dtype_code(mine), _ptr(mine), _numel(mine), mine_virtuals, _ptr(theirs),
+            _numel(theirs), theirs_virtuals, int(keep_high), _ptr(out), ctypes.byref(nr),
+            ctypes.byref(nv), B2S_HOST if host else B2S_DEVICE))
+        return out[: nr.value], nv.value
+
+    # -- sample sort steps (device tensors) -----------------------------------
+    def sample_regular(self, sorted_keys, rank: int, samples: int, out=None, stream=None):
+        """(samples, 2) uint64 tensor of (order key, rank<<40 | position) records."""
+        if out is None:
+            out = torch.empty((samples, 2), dtype=torch.uint64, device=sorted_keys.device)
+        self._bind_stream(stream)
+        check(lib().b2s_sample_regular(self._h, dtype_code(sorted_keys), _ptr(sorted_keys),
+                                       _numel(sorted_keys), rank, samples, _ptr(out)))
+        return out
+
+    def select_splitters(self, samples, nparts: int, out=None, stream=None):
+        count = samples.shape[0]
+        if out is None:
+            out = torch.empty((max(nparts - 1, 1), 2), dtype=torch.uint64, device=samples.device)
+        self._bind_stream(stream)
+        check(lib().b2s_select_splitters(self._h, _ptr(samples), count, nparts, _ptr(out)))
+        return out
+
+    def bucket_bounds(self, sorted_keys, rank: int, splitters, nparts: int, out=None,
+                      stream=None):
+        if out is None:
+            out = torch.empty(nparts + 1, dtype=torch.int64, device=sorted_keys.device)
+        self._bind_stream(stream)
+        check(lib().b2s_bucket_bounds(self._h, dtype_code(sorted_keys), _ptr(sorted_keys),
+                                      _numel(sorted_keys), rank, _ptr(splitters), nparts,
+                                      _ptr(out)))
+        return out
+
+    # -- generation / verification -------------------------------------------
+    def gen_keys(self, n: int, seed: int, dtype, shift: int = 0, first: int = 0, out=None,
+                 stream=None):
+        """bench::gen_data's stream on the device: key_i = (T)(z_{first+i} >> shift)."""
+        if out is None:
+            out = torch.empty(n, dtype=dtype, device=f"cuda:{self.device}")
+        self._bind_stream(stream)
+        check(lib().b2s_gen_keys(self._h, dtype_code(out), first, n, seed, shift, _ptr(out)))
+        return out
+
+    def check_sorted(self, keys, stream=None):
+        """(adjacent inversions, order-sensitive fingerprint, multiset hash)."""
+        inv, fp, ms = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self._bind_stream(stream)
+        check(lib().b2s_check_sorted(self._h, dtype_code(keys), _ptr(keys), _numel(keys),
+                                     ctypes.byref(inv), ctypes.byref(fp), ctypes.byref(ms)))
+        return inv.value, fp.value, ms.value
+
+    # -- helpers ----------------------------------------------------------------
+    @staticmethod
+    def _validate_pair(keys, out, vals, vals_out):
+        _check_1d(out, "out")
+        if _numel(out) != _numel(keys) or dtype_code(out) != dtype_code(keys):
+            raise ValueError("out must match keys in size and dtype")
+        if _is_host(out) != _is_host(keys):
+            raise ValueError("keys and out must live in the same memory space")
+        if (vals is None) != (vals_out is None):
+            raise ValueError("vals and vals_out go together")
+        if vals is not None:
+            _check_1d(vals, "vals")
+            _check_1d(vals_out, "vals_out")
+            if _numel(vals) != _numel(keys) or _numel(vals_out) != _numel(keys):
+                raise ValueError("vals must match keys in size")
+            for v in (vals, vals_out):
+                if isinstance(v, np.ndarray):
+                    ok = v.dtype in (np.uint32, np.int32)
+                else:
+                    ok = v.dtype in (torch.int32, torch.uint32)
+                if not ok:
+                    raise TypeError("the payload is 32-bit (uint32 / int32)")
+
+
+def _numel(x) -> int:
+    return int(x.size) if isinstance(x, np.ndarray) else int(x.numel())
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    """A lazily created per-device context for the module-level helpers."""
+    ctx = _default.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _default[device] = ctx
+    return ctx

@@ -1,0 +1,102 @@
+"""GPU: merge-path merges (b2s_merge, b2s_merge_split_padded) and the
+single-GPU partitioned sort against the oracle, including kernels::merge_runs'
+tie rule (ties from the lower run) checked through a payload."""
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1105_6040_b200.device import Context  # noqa: E402
+from test_gpu_sort import DTYPES, rand_keys, to_dev, to_host  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 7, 8, 9, 16])
+def test_kway_merge(ctx, dt, k):
+    rng = np.random.default_rng(k * 31 + np.dtype(dt).itemsize)
+    for kind in ("uniform", "dups"):
+        lens = [int(x) for x in rng.integers(0, 20_000, k)]
+        if k > 2:
+            lens[1] = 0  # an empty run in the middle
+        runs = [oracle.sort(rand_keys(n, dt, rng, kind)) for n in lens]
+        out, _ = ctx.merge([to_dev(r) for r in runs])
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out, dt), oracle.merge_kway(runs)), (kind, lens)
+        hout, _ = ctx.merge(runs)  # host buffers
+        assert np.array_equal(hout, oracle.merge_kway(runs))
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+def test_kway_merge_ties_take_lower_run(ctx, k):
+    """Stability: equal keys come out in run order, then position order
+    (merge_runs' rule, P/src/sort_core.cpp:46, tested at
+    P/tests/test_sort_core.cpp:110-120)."""
+    rng = np.random.default_rng(k)
+    runs, vals, off = [], [], 0
+    for _ in range(k):
+        n = int(rng.integers(1000, 30_000))
+        runs.append(np.sort(rng.integers(0, 8, n).astype(np.uint32)))
+        vals.append(np.arange(off, off + n, dtype=np.uint32))
+        off += n
+    ek, ev = oracle.stable_sort_kv(np.concatenate(runs), np.concatenate(vals))
+    ok, ov = ctx.merge([to_dev(r) for r in runs],
+                       vals=[torch.from_numpy(v.view(np.int32)).cuda() for v in vals])
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(ok, np.uint32), ek)
+    assert np.array_equal(ov.cpu().numpy().view(np.uint32), ev)
+
+
+def test_merge_runs_kats(ctx, golden):
+    for m in golden["merge_runs"]:
+        a = np.array(m["a"], dtype=np.int64)
+        b = np.array(m["b"], dtype=np.int64)
+        out, _ = ctx.merge([a, b])
+        assert out.tolist() == m["expected"]
+
+
+def test_merge_rejects_aliasing_output(ctx):
+    from paper_1105_6040_b200.errors import ConfigError
+    x = torch.arange(100, dtype=torch.int64, device="cuda")
+    with pytest.raises(ConfigError):
+        ctx.merge([x[:50], x[50:]], out=x)
+
+
+def test_merge_split_padded_golden(ctx, golden):
+    for c in golden["merge_split_padded"]:
+        reals, virt = ctx.merge_split_padded(np.array(c["mine"], dtype=np.int64),
+                                             c["mine_virt"],
+                                             np.array(c["theirs"], dtype=np.int64),
+                                             c["theirs_virt"], c["keep"] == "high")
+        assert reals.tolist() == c["reals"] and virt == c["virtuals"], c
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8, 13, 64])
+def test_partitioned_sort(ctx, dt, p):
+    rng = np.random.default_rng(p)
+    for n in (0, 5, 4097, 250_001):
+        keys = rand_keys(n, dt, rng, "uniform" if n % 2 else "dups")
+        out, _ = ctx.partitioned_sort(to_dev(keys), p)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out, dt), oracle.sort(keys)), (n, p)
+
+
+def test_partitioned_sort_pairs_stable(ctx):
+    rng = np.random.default_rng(4)
+    n = 300_000
+    keys = rng.integers(0, 100, n).astype(np.int64)
+    vals = np.arange(n, dtype=np.uint32)
+    ek, ev = oracle.stable_sort_kv(keys, vals)
+    for p in (1, 3, 4, 8):
+        ok, ov = ctx.partitioned_sort(keys, p, vals=vals)
+        assert np.array_equal(ok, ek) and np.array_equal(ov, ev), p
