@@ -77,7 +77,8 @@ typedef struct b2s_timing {
 /* ---- context ----------------------------------------------------------- */
 b2s_status b2s_create(int device, b2s_ctx** out);
 b2s_status b2s_destroy(b2s_ctx* ctx);
-/* `stream` is a cudaStream_t; NULL selects the context's own stream. */
+/* `stream` is a cudaStream_t (NULL = the legacy default stream). A new
+ * context starts on its own non-blocking stream. */
 b2s_status b2s_set_stream(b2s_ctx* ctx, void* stream);
 b2s_status b2s_synchronize(b2s_ctx* ctx);
 b2s_status b2s_enable_timing(b2s_ctx* ctx, int on);

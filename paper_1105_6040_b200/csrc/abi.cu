@@ -175,12 +175,7 @@ b2s_status b2s_create(int device, b2s_ctx** out) {
     }
     ctx->stream = ctx->own_stream;
     for (int i = 0; i < 40; ++i) cudaEventCreate(&ctx->ev[i]);
-    // the histogram buffer is self-cleaning after its first zeroing
-    b2s_status st = ctx->hist.ensure(kMaxSlots * 256 * sizeof(unsigned long long));
-    if (st == B2S_OK) {
-        e = cudaMemset(ctx->hist.ptr, 0, kMaxSlots * 256 * sizeof(unsigned long long));
-        if (e != cudaSuccess) st = set_error(B2S_ECUDA, "cudaMemset: %s", cudaGetErrorString(e));
-    }
+    b2s_status st = ctx->hist.ensure(sizeof(RadixCounters));
     if (st != B2S_OK) {
         b2s_destroy(ctx);
         return st;
@@ -209,7 +204,8 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
 
 b2s_status b2s_set_stream(b2s_ctx* ctx, void* stream) {
     B2S_TRY(check_ctx(ctx));
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    // CUDA convention: NULL is the legacy default stream (torch's default stream)
+    ctx->stream = static_cast<cudaStream_t>(stream);
     return B2S_OK;
 }
 

@@ -54,14 +54,17 @@ struct HostBuf {  // pinned
 
 enum { kMaxSlots = 8 };
 
-// Per-call radix sort plan, written on the device by radix_plan_kernel from the
-// upfront histogram so that constant-digit passes are skipped without a host
-// round trip. Slot s runs digit position digit[s]; slots >= num_active exit.
+// Per-call radix sort plan, written on the device by radix_plan_kernel from
+// the prologue's bit statistics so that constant-digit passes are skipped
+// without a host round trip. Slot s runs digit position digit[s]; slots >=
+// num_active exit at once.
 struct RadixPlan {
     int num_active;
     int do_copy;
+    int need_fallback;  // first active digit is not digit 0: recount it
     int digit[kMaxSlots];
     uint32_t dxor[kMaxSlots];  // 0x80 on the top digit of signed keys
+    const unsigned long long* hist[kMaxSlots];  // digit histogram per slot
     const void* ksrc[kMaxSlots];
     void* kdst[kMaxSlots];
     const uint32_t* vsrc[kMaxSlots];
@@ -71,7 +74,14 @@ struct RadixPlan {
     const uint32_t* copy_vsrc;
     uint32_t* copy_vdst;
     unsigned int tile_counter[kMaxSlots];
-    unsigned long long digit_offset[kMaxSlots][256];
+};
+
+// Device counters of one sort call, zeroed by one memset at the call's start.
+struct RadixCounters {
+    unsigned long long hist[kMaxSlots][256];  // slot s's digit histogram
+    unsigned long long spec0[256];            // prologue's digit-0 histogram
+    unsigned long long or_all;                // OR of all keys
+    unsigned long long nor_all;               // OR of all complemented keys
 };
 
 struct TimingEvents {

@@ -7,24 +7,30 @@
 // stable (equal keys keep input order, merge_sort's tie rule :77).
 //
 // Structure (one call, all on one stream, no host round trip):
-//   radix_hist_kernel   one read of the keys: 256-bin histograms of EVERY
-//                       8-bit digit position at once, and zeroes look-back
-//                       region 0.
-//   radix_plan_kernel   1 CTA: exclusive scan per digit position -> global
-//                       digit offsets; marks constant digits (one bin holds
-//                       all n keys) as skipped; assigns ping-pong buffers so
-//                       the last executed pass lands in the output.
-//   onesweep_kernel x S one launch per digit slot: persistent CTAs take tiles
-//                       from an atomic counter, rank keys in-warp with
-//                       __match_any_sync, publish per-digit tile counts, resolve
-//                       the tile's global offsets by decoupled look-back, stage
-//                       the tile digit-sorted in shared memory, and write runs
-//                       of equal digits with coalesced stores.
-//   radix_copy_kernel   only does work when an in-place sort executed an odd
-//                       number of passes (or zero passes out of place).
+//   radix_prologue_kernel  one read of the keys: OR / OR-of-complement of all
+//                          keys (which bits vary, hence which 8-bit digits are
+//                          constant and can be skipped) and the digit-0
+//                          histogram; zeroes look-back region 0.
+//   radix_plan_kernel      1 thread: active digit list, histogram source per
+//                          slot, ping-pong buffer chain so the last executed
+//                          pass lands in the output.
+//   radix_fallback_hist    recounts the first active digit when digit 0 is
+//                          constant (exits at once otherwise).
+//   onesweep_kernel x S    one launch per digit slot: persistent CTAs scan the
+//                          slot's histogram into global digit offsets, take
+//                          tiles from an atomic counter, count digits per warp
+//                          (shared reductions), publish per-digit tile counts,
+//                          rank keys in-warp with ballot-based digit matching,
+//                          resolve the tile's global offsets by decoupled
+//                          look-back, stage the tile digit-sorted in shared
+//                          memory, write runs of equal digits with coalesced
+//                          stores, and count the NEXT slot's digit on the way
+//                          out (so no all-digit histogram pass is needed).
+//   radix_copy_kernel      only does work when an in-place sort executed an
+//                          odd number of passes (or zero passes out of place).
 //
 // HBM traffic per executed pass: read + write of every key (and payload):
-// 2 * (key_bytes + val_bytes) * n. The histogram reads key_bytes * n once.
+// 2 * (key_bytes + val_bytes) * n. The prologue reads key_bytes * n once.
 #include <cub/warp/warp_scan.cuh>
 
 #include <stdlib.h>
@@ -75,110 +81,108 @@ __device__ __forceinline__ uint32_t digit_of(U k, int shift, uint32_t dxor) {
 }
 
 // ---------------------------------------------------------------------------
-// upfront histogram of all digit positions
+// prologue: varying-bit statistics + digit-0 histogram (one read of the keys)
+
+template <typename U, int D>
+__device__ __forceinline__ void prologue_keys(const U (&e)[D], unsigned long long& o,
+                                              unsigned long long& no, uint32_t hbase) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        o |= (unsigned long long)e[j];
+        no |= (unsigned long long)(U)~e[j];
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * ((uint32_t)e[j] & 0xFFu))
+                     : "memory");
+    }
+}
 
 template <typename U>
-__global__ void __launch_bounds__(512) radix_hist_kernel(const U* __restrict__ keys, uint64_t n,
-                                                         uint32_t top_xor,
-                                                         unsigned long long* __restrict__ g_hist,
-                                                         uint4* __restrict__ lb_zero,
-                                                         uint64_t lb_zero_vecs) {
-    constexpr int NP = sizeof(U);
+__global__ void __launch_bounds__(512) radix_prologue_kernel(const U* __restrict__ keys, uint64_t n,
+                                                             RadixCounters* __restrict__ ctr,
+                                                             uint4* __restrict__ lb_zero,
+                                                             uint64_t lb_zero_vecs) {
     constexpr int VEC = 16 / sizeof(U);
-    __shared__ uint32_t s_h[NP][kRadix];
-    for (int i = threadIdx.x; i < NP * kRadix; i += blockDim.x) (&s_h[0][0])[i] = 0;
+    __shared__ uint32_t s_h[kRadix];
+    __shared__ unsigned long long s_or[16], s_nor[16];
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) s_h[i] = 0;
     __syncthreads();
-
+    const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(s_h);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-
     for (uint64_t i = tid; i < lb_zero_vecs; i += stride) lb_zero[i] = make_uint4(0, 0, 0, 0);
 
-    // run-length aggregation per digit position: sorted / constant inputs
-    // collapse to a few shared-memory atomics instead of one per key
-    uint32_t cur[NP], cnt[NP];
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        cur[p] = 0;
-        cnt[p] = 0;
-    }
-    auto count_key = [&](U k) {
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            uint32_t d = (uint32_t)(k >> (8 * p)) & 0xFFu;
-            if (p == NP - 1) d ^= top_xor;
-            if (d == cur[p]) {
-                ++cnt[p];
-            } else {
-                if (cnt[p]) atomicAdd(&s_h[p][cur[p]], cnt[p]);
-                cur[p] = d;
-                cnt[p] = 1;
-            }
-        }
-    };
-
-    const uint64_t nvec = n / VEC;
-    const uint4* kv = reinterpret_cast<const uint4*>(keys);
+    unsigned long long o = 0, no = 0;
     const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+    uint64_t head = 0;
     if (aligned) {
-        for (uint64_t v = tid; v < nvec; v += stride) {
-            uint4 q = __ldcs(kv + v);
-            const U* e = reinterpret_cast<const U*>(&q);
+        const uint4* kv = reinterpret_cast<const uint4*>(keys);
+        const uint64_t nvec = n / VEC;
+        uint64_t v = tid;
+        for (; v + 3 * stride < nvec; v += 4 * stride) {  // 4 independent 16-B loads in flight
+            uint4 q[4];
 #pragma unroll
-            for (int j = 0; j < VEC; ++j) count_key(e[j]);
+            for (int u = 0; u < 4; ++u) q[u] = __ldcs(kv + v + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                prologue_keys<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q[u]), o, no, hbase);
         }
-        for (uint64_t i = nvec * VEC + tid; i < n; i += stride) count_key(keys[i]);
-    } else {
-        for (uint64_t i = tid; i < n; i += stride) count_key(keys[i]);
+        for (; v < nvec; v += stride) {
+            uint4 q = __ldcs(kv + v);
+            prologue_keys<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q), o, no, hbase);
+        }
+        head = nvec * VEC;
     }
+    for (uint64_t i = head + tid; i < n; i += stride) {
+        const U e[1] = {keys[i]};
+        prologue_keys<U, 1>(e, o, no, hbase);
+    }
+    // block OR-reduction, then one global atomic per block
 #pragma unroll
-    for (int p = 0; p < NP; ++p)
-        if (cnt[p]) atomicAdd(&s_h[p][cur[p]], cnt[p]);
+    for (int off = 16; off > 0; off >>= 1) {
+        o |= __shfl_xor_sync(0xffffffffu, o, off);
+        no |= __shfl_xor_sync(0xffffffffu, no, off);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s_or[warp] = o;
+        s_nor[warp] = no;
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < NP * kRadix; i += blockDim.x) {
-        const uint32_t c = (&s_h[0][0])[i];
-        if (c) atomicAdd(&g_hist[i], (unsigned long long)c);
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            o |= s_or[w];
+            no |= s_nor[w];
+        }
+        if (o) atomicOr(&ctr->or_all, o);
+        if (no) atomicOr(&ctr->nor_all, no);
+    }
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) {
+        const uint32_t c = s_h[i];
+        if (c) atomicAdd(&ctr->spec0[i], (unsigned long long)c);
     }
 }
 
 // ---------------------------------------------------------------------------
-// pass plan: global digit offsets, skipped digits, buffer chain
+// pass plan: active digits, histogram per slot, buffer chain
 
-__global__ void __launch_bounds__(256) radix_plan_kernel(
-    RadixPlan* __restrict__ plan, unsigned long long* __restrict__ g_hist, int np, uint64_t n,
-    uint32_t top_xor, const void* kin, void* kout, void* ktmp, const uint32_t* vin,
-    uint32_t* vout, uint32_t* vtmp) {
-    using WarpScan = cub::WarpScan<unsigned long long>;
-    __shared__ typename WarpScan::TempStorage ws[8];
-    __shared__ unsigned long long s_warp[8];
-    __shared__ int s_trivial[kMaxSlots];
-    const int d = threadIdx.x, warp = d >> 5, lane = d & 31;
-
-    for (int p = 0; p < np; ++p) {
-        const unsigned long long c = g_hist[p * kRadix + d];
-        g_hist[p * kRadix + d] = 0;  // self-cleaning for the next call
-        const int triv = __syncthreads_or(c == n);
-        unsigned long long incl;
-        WarpScan(ws[warp]).InclusiveSum(c, incl);
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        unsigned long long base = 0;
-        for (int w = 0; w < warp; ++w) base += s_warp[w];
-        plan->digit_offset[p][d] = base + incl - c;
-        if (d == 0) s_trivial[p] = triv || n == 0;
-        __syncthreads();
-    }
-    if (d < kMaxSlots) plan->tile_counter[d] = 0;
-    if (d != 0) return;
-
+__global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* __restrict__ ctr,
+                                  int np, uint64_t n, uint32_t top_xor, const void* kin,
+                                  void* kout, void* ktmp, const uint32_t* vin, uint32_t* vout,
+                                  uint32_t* vtmp) {
+    if (threadIdx.x < kMaxSlots) plan->tile_counter[threadIdx.x] = 0;
+    if (threadIdx.x != 0) return;
+    // a bit varies iff some key has it set and some key has it clear
+    const unsigned long long varying = ctr->or_all & ctr->nor_all;
     int na = 0;
-    for (int p = 0; p < np; ++p) {
-        if (s_trivial[p]) continue;
+    for (int p = 0; p < np && n > 0; ++p) {
+        if (((varying >> (8 * p)) & 0xFFull) == 0) continue;  // constant digit: identity pass
         plan->digit[na] = p;
         plan->dxor[na] = (p == np - 1) ? top_xor : 0u;
+        plan->hist[na] = ctr->hist[na];
         ++na;
     }
     plan->num_active = na;
+    plan->need_fallback = (na > 0 && plan->digit[0] != 0);
+    if (na > 0 && plan->digit[0] == 0) plan->hist[0] = ctr->spec0;
     // Buffer chain: slot s writes `out` when (na-1-s) is even, else `tmp`, so
     // the last executed slot always lands in `out`. When in == out and na is
     // odd, slot 0 cannot write `out` (it is reading it): the chain then runs
@@ -213,6 +217,26 @@ __global__ void __launch_bounds__(256) radix_plan_kernel(
     plan->copy_vdst = vout;
 }
 
+// Histogram of the first active digit when it is not digit 0.
+template <typename U>
+__global__ void __launch_bounds__(512) radix_fallback_hist_kernel(const RadixPlan* __restrict__ plan,
+                                                                  const U* __restrict__ keys,
+                                                                  uint64_t n,
+                                                                  RadixCounters* __restrict__ ctr) {
+    if (!plan->need_fallback) return;
+    __shared__ uint32_t s_h[kRadix];
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) s_h[i] = 0;
+    __syncthreads();
+    const int shift = 8 * plan->digit[0];
+    const uint32_t dxor = plan->dxor[0];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        atomicAdd(&s_h[digit_of(keys[i], shift, dxor)], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x)
+        if (s_h[i]) atomicAdd(&ctr->hist[0][i], (unsigned long long)s_h[i]);
+}
+
 // ---------------------------------------------------------------------------
 // onesweep digit pass
 
@@ -226,178 +250,293 @@ struct OnesweepSmem {
     static constexpr size_t bytes = kWhist + kKeys + kVals;
 };
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __restrict__ plan, int slot,
-                                                           uint64_t n, uint32_t ntiles,
-                                                           LB* __restrict__ lb_cur,
-                                                           LB* __restrict__ lb_next) {
-    using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
-    using W = LookbackWord<LB>;
-    constexpr int WARPS = SM::WARPS;
-    constexpr int TILE = SM::TILE;
-    constexpr int WSEG = 32 * ITEMS;
-    static_assert(THREADS >= kRadix, "one thread per digit is required");
-    static_assert(TILE <= 65536, "tile ranks are kept in 16 bits");
+// Lanes of the warp whose digit equals mine, from one ballot per digit bit
+// (VOTE + logic ops only: MATCH.ANY and FLO serialise on the SM's shared
+// ADU/XU pipes, which capped the first version at ~1 TB/s).
+template <int BITS>
+__device__ __forceinline__ uint32_t match_digit(uint32_t d) {
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < BITS; ++b) {
+        uint32_t m;
+        asm("{\n\t.reg .pred p;\n\t"
+            "and.b32 %0, %1, %2;\n\t"
+            "setp.ne.u32 p, %0, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "@!p not.b32 %0, %0;\n\t}"
+            : "=r"(m)
+            : "r"(d), "r"(1u << b));
+        peers &= m;
+    }
+    return peers;
+}
 
-    if (slot >= plan->num_active) return;
+// 32-bit shared-window addressing: computed once, so the per-key shared
+// accesses below cost one address add instead of a generic->shared conversion.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u32_if(bool pred, uint32_t a, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.volatile.shared.u32 [%0], %1;\n\t}"
+                 ::"r"(a), "r"(v), "r"((uint32_t)pred) : "memory");
+}
+__device__ __forceinline__ void red_add_shared(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_key(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_key(uint32_t a, unsigned long long v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+struct NextDigit {
+    int shift;
+    uint32_t dxor;
+    bool on;
+    uint32_t hist_a;  // shared address of the next slot's digit counters
+};
+
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL>
+__device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid, uint64_t tile_base,
+                                              const U* __restrict__ src, U* __restrict__ dst,
+                                              const uint32_t* __restrict__ vsrc,
+                                              uint32_t* __restrict__ vdst,
+                                              const unsigned long long* s_goff,
+                                              LB* __restrict__ lb_cur, int shift, uint32_t dxor,
+                                              const NextDigit nd, uint32_t* s_whist, U* s_keys,
+                                              uint32_t* s_vals, unsigned long long* s_gbase,
+                                              uint32_t* s_wsum) {
+    using W = LookbackWord<LB>;
+    constexpr int WARPS = THREADS / 32;
+    constexpr int WSEG = 32 * ITEMS;
+    constexpr int LOOKBACK = 4;  // predecessors read per look-back step
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const uint32_t wh_a = smem_addr(s_whist + warp * kRadix);
+    const uint32_t keys_a = smem_addr(s_keys);
+    const uint32_t vals_a = smem_addr(s_vals);
+
+    // ---- load: warp w owns keys [w*WSEG, (w+1)*WSEG) of the tile; item j of
+    // lane l is key j*32+l (coalesced; in-warp order == input order)
+    U keys[ITEMS];
+    uint32_t vals[VALS ? ITEMS : 1];
+    const uint32_t wbase = warp * WSEG;
+    const U* wsrc = src + tile_base + wbase + lane;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        if (FULL) keys[j] = __ldcs(wsrc + j * 32);
+        else keys[j] = (wbase + j * 32 + lane < tile_valid) ? wsrc[j * 32] : U(0);
+    }
+    if constexpr (VALS) {
+        const uint32_t* wv = vsrc + tile_base + wbase + lane;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (FULL) vals[j] = __ldcs(wv + j * 32);
+            else vals[j] = (wbase + j * 32 + lane < tile_valid) ? wv[j * 32] : 0u;
+        }
+    }
+
+    // ---- early counts: per-warp digit histogram with shared reductions
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t a = wh_a + 4 * digit_of(keys[j], shift, dxor);
+        if (FULL) red_add_shared(a, 1u);
+        else if (wbase + j * 32 + lane < tile_valid) red_add_shared(a, 1u);
+    }
+    __syncthreads();
+
+    // ---- per digit: exclusive prefix over warps, tile count, publish early
+    uint32_t count = 0, start = 0;
+    if (tid < kRadix) {
+#pragma unroll 4
+        for (int w = 0; w < WARPS; ++w) {
+            const uint32_t c = s_whist[w * kRadix + tid];
+            s_whist[w * kRadix + tid] = count;
+            count += c;
+        }
+        st_relaxed(lb_cur + (size_t)tile * kRadix + tid, (tile == 0 ? W::kInc : W::kAgg) | (LB)count);
+        uint32_t incl = count;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        start = incl - count;
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+#pragma unroll
+        for (int w = 0; w < kRadix / 32; ++w) start += (w < warp) ? s_wsum[w] : 0u;
+#pragma unroll 4
+        for (int w = 0; w < WARPS; ++w) s_whist[w * kRadix + tid] += start;
+    }
+    __syncthreads();
+
+    // ---- rank within the tile and stage digit-sorted in shared memory. The
+    // warp's counters start at its offset for each digit; item j of lane l
+    // precedes item j of lane l+1 and item j+1 of any lane (input order), so
+    // ranks are stable. The highest peer advances the counter. A warp's
+    // shared accesses are performed in program order and the loop has no
+    // divergent branch, so item j+1 reads item j's update without a barrier.
+    const uint32_t lanemask_lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const bool valid = FULL || (wbase + j * 32 + lane < tile_valid);
+        const uint32_t d = valid ? digit_of(keys[j], shift, dxor) : (uint32_t)kRadix;
+        const uint32_t peers = match_digit<FULL ? 8 : 9>(d);
+        const uint32_t below = __popc(peers & lanemask_lt);
+        const bool leader = (peers >> lane) == 1u;
+        const uint32_t ca = wh_a + 4 * (d & (kRadix - 1));
+        const uint32_t r = lds_u32(ca) + below;
+        sts_u32_if(valid && leader, ca, r + 1);
+        if (valid) {
+            sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j]);
+            if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j]);
+        }
+    }
+
+    // ---- decoupled look-back: one lane per digit, LOOKBACK predecessors per
+    // step (independent loads), warp-uniform loop
+    if (tid < kRadix) {
+        unsigned long long excl = 0;
+        if (tile > 0) {
+            int64_t pred = (int64_t)tile - 1;
+            bool done = false;
+            const LB* col = lb_cur + tid;
+            while (__any_sync(0xffffffffu, !done)) {
+                if (!done) {
+                    LB w[LOOKBACK];
+#pragma unroll
+                    for (int i = 0; i < LOOKBACK; ++i)
+                        w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * kRadix) : W::kInc;
+                    bool stop = false;
+#pragma unroll
+                    for (int i = 0; i < LOOKBACK; ++i) {
+                        const LB f = W::flag(w[i]);
+                        if (!stop && f != 0) {
+                            excl += (unsigned long long)(w[i] & W::kMask);
+                            done = (f == 2);
+                            stop = done;
+                            pred -= done ? 0 : 1;
+                        } else {
+                            stop = true;
+                        }
+                    }
+                }
+            }
+            st_relaxed(lb_cur + (size_t)tile * kRadix + tid, W::kInc | (LB)(excl + count));
+        }
+        s_gbase[tid] = s_goff[tid] + excl - start;
+    }
+    __syncthreads();
+
+    // ---- write runs of equal digits: consecutive threads, consecutive slots;
+    // count the next slot's digit on the way out
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = j * THREADS + tid;
+        if (FULL || i < tile_valid) {
+            const U k = s_keys[i];
+            const unsigned long long g = s_gbase[digit_of(k, shift, dxor)] + i;
+            __stcs(dst + g, k);
+            if constexpr (VALS) __stcs(vdst + g, s_vals[i]);
+            if (nd.on) red_add_shared(nd.hist_a + 4 * digit_of(k, nd.shift, nd.dxor), 1u);
+        }
+    }
+}
+
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __restrict__ plan,
+                                                                 RadixCounters* __restrict__ ctr,
+                                                                 int slot, uint64_t n,
+                                                                 uint32_t ntiles,
+                                                                 LB* __restrict__ lb_cur,
+                                                                 LB* __restrict__ lb_next) {
+    using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
+    constexpr int TILE = SM::TILE;
+    static_assert(THREADS >= kRadix, "one thread per digit is required");
+
+    const int na = plan->num_active;
+    if (slot >= na) return;
 
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem);
     U* s_keys = reinterpret_cast<U*>(smem + SM::kWhist);
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem + SM::kWhist + SM::kKeys);
     __shared__ unsigned long long s_gbase[kRadix];
-    __shared__ uint32_t s_start[kRadix];
+    __shared__ unsigned long long s_goff[kRadix];
+    __shared__ uint32_t s_nhist[kRadix];
+    __shared__ unsigned long long s_wsum64[kRadix / 32];
     __shared__ uint32_t s_wsum[kRadix / 32];
     __shared__ uint32_t s_tile;
 
-    const int digit_pos = plan->digit[slot];
-    const int shift = 8 * digit_pos;
-    const uint32_t dxor = plan->dxor[slot];
-    const U* __restrict__ src = static_cast<const U*>(plan->ksrc[slot]);
-    U* __restrict__ dst = static_cast<U*>(plan->kdst[slot]);
-    const uint32_t* __restrict__ vsrc = plan->vsrc[slot];
-    uint32_t* __restrict__ vdst = plan->vdst[slot];
-    const unsigned long long* __restrict__ goff = plan->digit_offset[digit_pos];
-
     const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    const uint32_t lanemask_lt = (1u << lane) - 1u;
-    uint32_t* wh = s_whist + warp * kRadix;
+    const int shift = 8 * plan->digit[slot];
+    const uint32_t dxor = plan->dxor[slot];
+    const U* src = static_cast<const U*>(plan->ksrc[slot]);
+    U* dst = static_cast<U*>(plan->kdst[slot]);
+    const uint32_t* vsrc = plan->vsrc[slot];
+    uint32_t* vdst = plan->vdst[slot];
+    NextDigit nd;
+    nd.on = slot + 1 < na;
+    nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
+    nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
+    nd.hist_a = smem_addr(s_nhist);
 
+    // global digit offsets of this slot: exclusive scan of its histogram
+    if (tid < kRadix) {
+        const unsigned long long c = plan->hist[slot][tid];
+        unsigned long long incl = c;
+        const int lane = tid & 31;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_wsum64[tid >> 5] = incl;
+        s_goff[tid] = incl - c;
+        s_nhist[tid] = 0;
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+        unsigned long long base = 0;
+#pragma unroll
+        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? s_wsum64[w] : 0ull;
+        s_goff[tid] += base;
+    }
+
+    uint32_t* wh = s_whist + (tid >> 5) * kRadix;
     for (;;) {
         if (tid == 0) s_tile = atomicAdd(&plan->tile_counter[slot], 1u);
 #pragma unroll
-        for (int i = lane; i < kRadix; i += 32) wh[i] = 0;
+        for (int i = tid & 31; i < kRadix; i += 32) wh[i] = 0;
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= ntiles) break;
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
-        const uint32_t tile_valid = rem < (uint64_t)TILE ? (uint32_t)rem : (uint32_t)TILE;
-        if (lb_next != nullptr && tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
-
-        // ---- load: warp w owns keys [w*WSEG, (w+1)*WSEG) of the tile,
-        // item j of lane l is key j*32+l (coalesced, and in-warp order == input order)
-        U keys[ITEMS];
-        uint32_t vals[VALS ? ITEMS : 1];
-        const uint32_t wbase = warp * WSEG;
-        if (tile_valid == TILE) {
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) keys[j] = __ldcs(src + tile_base + wbase + j * 32 + lane);
-            if constexpr (VALS) {
-#pragma unroll
-                for (int j = 0; j < ITEMS; ++j)
-                    vals[j] = __ldcs(vsrc + tile_base + wbase + j * 32 + lane);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                const uint32_t idx = wbase + j * 32 + lane;
-                keys[j] = idx < tile_valid ? src[tile_base + idx] : U(0);
-                if constexpr (VALS) vals[j] = idx < tile_valid ? vsrc[tile_base + idx] : 0u;
-            }
-        }
-
-        // ---- warp-private ranking: peers with the same digit via match_any,
-        // the highest peer bumps the warp's counter for that digit
-        uint16_t rank[ITEMS];
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint32_t idx = wbase + j * 32 + lane;
-            const bool valid = idx < tile_valid;
-            const uint32_t d = valid ? digit_of(keys[j], shift, dxor) : (uint32_t)kRadix;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const int leader = 31 - __clz(peers);
-            uint32_t old = 0;
-            if (valid && lane == leader) {
-                old = wh[d];
-                wh[d] = old + __popc(peers);
-            }
-            old = __shfl_sync(0xffffffffu, old, leader);
-            rank[j] = (uint16_t)(old + __popc(peers & lanemask_lt));
-            __syncwarp();
-        }
-        __syncthreads();
-
-        // ---- per digit: exclusive prefix over warps, tile count, publish
-        uint32_t count = 0;
-        if (tid < kRadix) {
-#pragma unroll 4
-            for (int w = 0; w < WARPS; ++w) {
-                const uint32_t c = s_whist[w * kRadix + tid];
-                s_whist[w * kRadix + tid] = count;
-                count += c;
-            }
-            LB* slotp = lb_cur + (size_t)tile * kRadix + tid;
-            st_relaxed(slotp, (tile == 0 ? W::kInc : W::kAgg) | (LB)count);
-            // exclusive scan of the 256 tile counts (8 warps)
-            uint32_t incl = count;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (lane == 31) s_wsum[warp] = incl;
-            s_start[tid] = incl - count;  // partial (within warp)
-        }
-        __syncthreads();
-        if (tid < kRadix) {
-            uint32_t base = 0;
-#pragma unroll
-            for (int w = 0; w < kRadix / 32; ++w) base += (w < warp) ? s_wsum[w] : 0u;
-            const uint32_t start = s_start[tid] + base;
-            s_start[tid] = start;
-#pragma unroll 4
-            for (int w = 0; w < WARPS; ++w) s_whist[w * kRadix + tid] += start;
-        }
-        __syncthreads();
-
-        // ---- stage the tile digit-sorted in shared memory
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint32_t idx = wbase + j * 32 + lane;
-            if (idx < tile_valid) {
-                const uint32_t d = digit_of(keys[j], shift, dxor);
-                const uint32_t r = rank[j] + wh[d];
-                s_keys[r] = keys[j];
-                if constexpr (VALS) s_vals[r] = vals[j];
-            }
-        }
-
-        // ---- decoupled look-back: one thread per digit
-        if (tid < kRadix) {
-            unsigned long long excl = 0;
-            if (tile > 0) {
-                int64_t pred = (int64_t)tile - 1;
-                const LB* col = lb_cur + tid;
-                for (;;) {
-                    const LB w = ld_relaxed(col + (size_t)pred * kRadix);
-                    const LB f = W::flag(w);
-                    if (f == 0) continue;
-                    excl += (unsigned long long)(w & W::kMask);
-                    if (f == 2) break;
-                    --pred;
-                }
-                st_relaxed(lb_cur + (size_t)tile * kRadix + tid, W::kInc | (LB)(excl + count));
-            }
-            s_gbase[tid] = goff[tid] + excl - s_start[tid];
-        }
-        __syncthreads();
-
-        // ---- write runs of equal digits: consecutive threads, consecutive slots
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint32_t i = j * THREADS + tid;
-            if (i < tile_valid) {
-                const U k = s_keys[i];
-                const unsigned long long g = s_gbase[digit_of(k, shift, dxor)] + i;
-                dst[g] = k;
-                if constexpr (VALS) vdst[g] = s_vals[i];
-            }
-        }
+        if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
+        if (rem >= (uint64_t)TILE)
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, true>(
+                tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
+                s_whist, s_keys, s_vals, s_gbase, s_wsum);
+        else
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false>(
+                tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor,
+                nd, s_whist, s_keys, s_vals, s_gbase, s_wsum);
         __syncthreads();
     }
+    // hand the next slot's digit counts to global memory once per CTA
+    if (nd.on && tid < kRadix && s_nhist[tid])
+        atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)s_nhist[tid]);
 }
 
 template <typename U>
@@ -431,7 +570,8 @@ int onesweep_cfg() {
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
-b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, uint64_t n, void* lb) {
+b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
+                             void* lb) {
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
     auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB>;
@@ -450,7 +590,7 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, uint64_t n, void* lb
     const int slots = (int)sizeof(U);
     for (int s = 0; s < slots; ++s) {
         ctx->ev_pass[s] = record(ctx);
-        kern<<<grid, THREADS, SM::bytes, ctx->stream>>>(plan, s, n, ntiles, region[s & 1],
+        kern<<<grid, THREADS, SM::bytes, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
                                                       region[(s + 1) & 1]);
         B2S_LAUNCHED();
     }
@@ -462,16 +602,19 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, uint64_t n, void* lb
 constexpr int kMinTile = 256 * 12;
 
 template <typename U, bool VALS, typename LB>
-b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, uint64_t n, void* lb) {
+b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
     const int cfg = onesweep_cfg();
-    if constexpr (sizeof(U) == 4) {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, n, lb);
-        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, n, lb);
-        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, n, lb);
+    if constexpr (sizeof(U) == 4 && VALS) {
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
+    } else if constexpr (sizeof(U) == 4) {
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
+        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
     } else {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 4>(ctx, plan, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, n, lb);
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 4>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     }
 }
 
@@ -491,30 +634,37 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     B2S_TRY(ctx->lookback.ensure(2 * lb_region + 16));
     B2S_TRY(ctx->plan.ensure(sizeof(RadixPlan)));
     RadixPlan* plan = static_cast<RadixPlan*>(ctx->plan.ptr);
-    unsigned long long* hist = static_cast<unsigned long long*>(ctx->hist.ptr);
 
+    RadixCounters* ctr = static_cast<RadixCounters*>(ctx->hist.ptr);
     ctx->ev_hist0 = record(ctx);
+    B2S_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RadixCounters), ctx->stream));
     {
         const int threads = 512;
         uint64_t want = (n / (16 / sizeof(U)) + threads - 1) / threads;
         int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)ctx->num_sms * 4);
-        radix_hist_kernel<U><<<grid, threads, 0, ctx->stream>>>(
-            static_cast<const U*>(kin), n, top_xor, hist, static_cast<uint4*>(ctx->lookback.ptr),
+        radix_prologue_kernel<U><<<grid, threads, 0, ctx->stream>>>(
+            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(ctx->lookback.ptr),
             (lb_region + 15) / 16);
         B2S_LAUNCHED();
     }
-    radix_plan_kernel<<<1, 256, 0, ctx->stream>>>(plan, hist, NP, n, top_xor, kin, kout,
-                                                  ctx->alt_keys.ptr, vin, vout,
-                                                  static_cast<uint32_t*>(ctx->alt_vals.ptr));
+    radix_plan_kernel<<<1, 32, 0, ctx->stream>>>(plan, ctr, NP, n, top_xor, kin, kout,
+                                                 ctx->alt_keys.ptr, vin, vout,
+                                                 static_cast<uint32_t*>(ctx->alt_vals.ptr));
     B2S_LAUNCHED();
+    if (n > 0) {
+        int grid = (int)std::min<uint64_t>((n + 511) / 512, (uint64_t)ctx->num_sms * 4);
+        radix_fallback_hist_kernel<U><<<grid, 512, 0, ctx->stream>>>(plan, static_cast<const U*>(kin),
+                                                                     n, ctr);
+        B2S_LAUNCHED();
+    }
     ctx->ev_hist1 = record(ctx);
     ctx->last_passes_possible = NP;
 
     if (n > 0) {
         if (wide)
-            B2S_TRY((launch_passes<U, VALS, unsigned long long>(ctx, plan, n, ctx->lookback.ptr)));
+            B2S_TRY((launch_passes<U, VALS, unsigned long long>(ctx, plan, ctr, n, ctx->lookback.ptr)));
         else
-            B2S_TRY((launch_passes<U, VALS, uint32_t>(ctx, plan, n, ctx->lookback.ptr)));
+            B2S_TRY((launch_passes<U, VALS, uint32_t>(ctx, plan, ctr, n, ctx->lookback.ptr)));
     }
     {
         int grid = (int)std::min<uint64_t>(std::max<uint64_t>((n + 1023) / 1024, 1),
@@ -530,7 +680,7 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
 
 b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout,
                       const uint32_t* vin, uint32_t* vout, uint64_t n) {
-    B2S_TRY(ctx->hist.ensure(kMaxSlots * kRadix * sizeof(unsigned long long)));
+    B2S_TRY(ctx->hist.ensure(sizeof(RadixCounters)));
     const bool sgn = key_signed(dtype);
     const bool vals = vin != nullptr;
     if (key_bytes(dtype) == 4) {

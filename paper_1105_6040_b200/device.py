@@ -110,10 +110,10 @@ class Context:
     def _bind_stream(self, stream=None) -> None:
         if stream is None and torch is not None and torch.cuda.is_available():
             stream = torch.cuda.current_stream(self.device)
-        s = None
-        if stream is not None:
-            s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        check(lib().b2s_set_stream(self._h, s))
+        if stream is None:
+            return  # keep the context's own stream (no torch / no CUDA torch)
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        check(lib().b2s_set_stream(self._h, s or None))
 
     def synchronize(self) -> None:
         check(lib().b2s_synchronize(self._h))

@@ -41,6 +41,13 @@ def rand_keys(n, dt, rng, kind="uniform"):
     if kind == "topbyte":
         shift = np.dtype(dt).itemsize * 8 - 8
         return (rng.integers(0, 256, n).astype(np.uint64) << np.uint64(shift)).astype(dt)
+    if kind == "lowzero":  # digit 0 constant: the first active digit is recounted
+        return (rng.integers(info.min, info.max, n, dtype=dt, endpoint=True) & ~dt(0xFF)).astype(dt)
+    if kind == "midconst":  # a constant digit between varying ones
+        ut = np.uint32 if np.dtype(dt).itemsize == 4 else np.uint64
+        shift = ut(np.dtype(dt).itemsize * 8 - 16)
+        x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True).view(ut)
+        return (x & ~(ut(0xFF) << shift)).view(dt)
     if kind == "extremes":
         return rng.choice(np.array([info.min, info.max, 0, 1, info.max - 1, info.min + 1],
                                    dtype=dt), n)
@@ -70,7 +77,8 @@ def test_sort_uniform_sizes(ctx, dt, n):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
-@pytest.mark.parametrize("kind", ["dups", "equal", "sorted", "reverse", "topbyte", "extremes"])
+@pytest.mark.parametrize("kind", ["dups", "equal", "sorted", "reverse", "topbyte", "extremes",
+                                  "lowzero", "midconst"])
 def test_sort_distributions(ctx, dt, kind):
     rng = np.random.default_rng(5)
     for n in (5000, 70_001):
