@@ -245,10 +245,39 @@ struct OnesweepSmem {
     static constexpr int WARPS = THREADS / 32;
     static constexpr int TILE = THREADS * ITEMS;
     static constexpr size_t kWhist = (size_t)WARPS * kRadix * 4;
-    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);
+    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);  // one tile buffer
     static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
-    static constexpr size_t bytes = kWhist + kKeys + kVals;
+    // whist | keys[2] | vals[2]: tile i+1 streams in by TMA while tile i is
+    // ranked in place in its own buffer
+    static constexpr size_t bytes = kWhist + 2 * kKeys + 2 * kVals;
 };
+
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier ----------
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(mbar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // Lanes of the warp whose digit equals mine, from one ballot per digit bit
 // (VOTE + logic ops only: MATCH.ANY and FLO serialise on the SM's shared
@@ -302,15 +331,18 @@ struct NextDigit {
     uint32_t hist_a;  // shared address of the next slot's digit counters
 };
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL>
+// One tile: keys come from `kbuf` (already landed by TMA) when FROM_SMEM,
+// else straight from global memory; the tile is then ranked, staged
+// digit-sorted back into `kbuf`/`vbuf`, and written out.
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM>
 __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid, uint64_t tile_base,
                                               const U* __restrict__ src, U* __restrict__ dst,
                                               const uint32_t* __restrict__ vsrc,
                                               uint32_t* __restrict__ vdst,
                                               const unsigned long long* s_goff,
                                               LB* __restrict__ lb_cur, int shift, uint32_t dxor,
-                                              const NextDigit nd, uint32_t* s_whist, U* s_keys,
-                                              uint32_t* s_vals, unsigned long long* s_gbase,
+                                              const NextDigit nd, uint32_t* s_whist, U* kbuf,
+                                              uint32_t* vbuf, unsigned long long* s_gbase,
                                               uint32_t* s_wsum) {
     using W = LookbackWord<LB>;
     constexpr int WARPS = THREADS / 32;
@@ -320,26 +352,35 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const uint32_t wh_a = smem_addr(s_whist + warp * kRadix);
-    const uint32_t keys_a = smem_addr(s_keys);
-    const uint32_t vals_a = smem_addr(s_vals);
+    const uint32_t keys_a = smem_addr(kbuf);
+    const uint32_t vals_a = smem_addr(vbuf);
 
     // ---- load: warp w owns keys [w*WSEG, (w+1)*WSEG) of the tile; item j of
-    // lane l is key j*32+l (coalesced; in-warp order == input order)
+    // lane l is key j*32+l (coalesced / conflict-free; in-warp order == input order)
     U keys[ITEMS];
     uint32_t vals[VALS ? ITEMS : 1];
     const uint32_t wbase = warp * WSEG;
-    const U* wsrc = src + tile_base + wbase + lane;
+    if constexpr (FROM_SMEM) {
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        if (FULL) keys[j] = __ldcs(wsrc + j * 32);
-        else keys[j] = (wbase + j * 32 + lane < tile_valid) ? wsrc[j * 32] : U(0);
-    }
-    if constexpr (VALS) {
-        const uint32_t* wv = vsrc + tile_base + wbase + lane;
+        for (int j = 0; j < ITEMS; ++j) keys[j] = kbuf[wbase + j * 32 + lane];
+        if constexpr (VALS) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) vals[j] = vbuf[wbase + j * 32 + lane];
+        }
+    } else {
+        const U* wsrc = src + tile_base + wbase + lane;
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
-            if (FULL) vals[j] = __ldcs(wv + j * 32);
-            else vals[j] = (wbase + j * 32 + lane < tile_valid) ? wv[j * 32] : 0u;
+            if (FULL) keys[j] = __ldcs(wsrc + j * 32);
+            else keys[j] = (wbase + j * 32 + lane < tile_valid) ? wsrc[j * 32] : U(0);
+        }
+        if constexpr (VALS) {
+            const uint32_t* wv = vsrc + tile_base + wbase + lane;
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                if (FULL) vals[j] = __ldcs(wv + j * 32);
+                else vals[j] = (wbase + j * 32 + lane < tile_valid) ? wv[j * 32] : 0u;
+            }
         }
     }
 
@@ -350,7 +391,7 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
         if (FULL) red_add_shared(a, 1u);
         else if (wbase + j * 32 + lane < tile_valid) red_add_shared(a, 1u);
     }
-    __syncthreads();
+    __syncthreads();  // also: every warp has read its keys out of kbuf
 
     // ---- per digit: exclusive prefix over warps, tile count, publish early
     uint32_t count = 0, start = 0;
@@ -439,15 +480,17 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
     __syncthreads();
 
     // ---- write runs of equal digits: consecutive threads, consecutive slots;
-    // count the next slot's digit on the way out
+    // count the next slot's digit on the way out; clear this warp's counters
+#pragma unroll
+    for (int i = lane; i < kRadix; i += 32) s_whist[warp * kRadix + i] = 0;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t i = j * THREADS + tid;
         if (FULL || i < tile_valid) {
-            const U k = s_keys[i];
+            const U k = kbuf[i];
             const unsigned long long g = s_gbase[digit_of(k, shift, dxor)] + i;
             __stcs(dst + g, k);
-            if constexpr (VALS) __stcs(vdst + g, s_vals[i]);
+            if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
             if (nd.on) red_add_shared(nd.hist_a + 4 * digit_of(k, nd.shift, nd.dxor), 1u);
         }
     }
@@ -467,16 +510,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     const int na = plan->num_active;
     if (slot >= na) return;
 
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem);
-    U* s_keys = reinterpret_cast<U*>(smem + SM::kWhist);
-    uint32_t* s_vals = reinterpret_cast<uint32_t*>(smem + SM::kWhist + SM::kKeys);
+    U* kbuf[2] = {reinterpret_cast<U*>(smem + SM::kWhist),
+                  reinterpret_cast<U*>(smem + SM::kWhist + SM::kKeys)};
+    uint32_t* vbuf[2] = {reinterpret_cast<uint32_t*>(smem + SM::kWhist + 2 * SM::kKeys),
+                         reinterpret_cast<uint32_t*>(smem + SM::kWhist + 2 * SM::kKeys + SM::kVals)};
     __shared__ unsigned long long s_gbase[kRadix];
     __shared__ unsigned long long s_goff[kRadix];
     __shared__ uint32_t s_nhist[kRadix];
     __shared__ unsigned long long s_wsum64[kRadix / 32];
     __shared__ uint32_t s_wsum[kRadix / 32];
-    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_tile[2];
+    __shared__ alignas(8) unsigned long long s_mbar[2];
 
     const int tid = threadIdx.x;
     const int shift = 8 * plan->digit[slot];
@@ -490,6 +536,21 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
     nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
     nd.hist_a = smem_addr(s_nhist);
+    // TMA needs 16-byte aligned global sources (tiles are 16-byte multiples)
+    const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                     (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
+    const uint32_t mbar_a[2] = {smem_addr(&s_mbar[0]), smem_addr(&s_mbar[1])};
+    const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
+
+    auto prefetch = [&](uint32_t t, int b) {  // thread 0 only
+        if (tma && t < ntiles && n - (uint64_t)t * TILE >= (uint64_t)TILE) {
+            fence_proxy_async();
+            mbar_expect_tx(mbar_a[b], tx_bytes);
+            bulk_g2s(smem_addr(kbuf[b]), src + (uint64_t)t * TILE, (uint32_t)SM::kKeys, mbar_a[b]);
+            if constexpr (VALS)
+                bulk_g2s(smem_addr(vbuf[b]), vsrc + (uint64_t)t * TILE, (uint32_t)SM::kVals, mbar_a[b]);
+        }
+    };
 
     // global digit offsets of this slot: exclusive scan of its histogram
     if (tid < kRadix) {
@@ -505,6 +566,15 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         s_goff[tid] = incl - c;
         s_nhist[tid] = 0;
     }
+    for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_whist[i] = 0;
+    if (tid == 0) {
+        mbar_init(mbar_a[0], 1);
+        mbar_init(mbar_a[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
+        s_tile[0] = t;
+        prefetch(t, 0);
+    }
     __syncthreads();
     if (tid < kRadix) {
         unsigned long long base = 0;
@@ -513,26 +583,38 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         s_goff[tid] += base;
     }
 
-    uint32_t* wh = s_whist + (tid >> 5) * kRadix;
+    int cur = 0;
+    uint32_t parity = 0;  // bit b: phase parity of buffer b's mbarrier
     for (;;) {
-        if (tid == 0) s_tile = atomicAdd(&plan->tile_counter[slot], 1u);
-#pragma unroll
-        for (int i = tid & 31; i < kRadix; i += 32) wh[i] = 0;
-        __syncthreads();
-        const uint32_t tile = s_tile;
+        const uint32_t tile = s_tile[cur];
         if (tile >= ntiles) break;
+        if (tid == 0) {  // claim the next tile and start streaming it in
+            const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
+            s_tile[cur ^ 1] = t;
+            prefetch(t, cur ^ 1);
+        }
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
         if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
-        if (rem >= (uint64_t)TILE)
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, true>(
-                tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
-                s_whist, s_keys, s_vals, s_gbase, s_wsum);
-        else
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false>(
+        if (rem >= (uint64_t)TILE) {
+            if (tma) {
+                mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
+                parity ^= 1u << cur;
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true>(
+                    tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
+                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum);
+            } else {
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false>(
+                    tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
+                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum);
+            }
+        } else {
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false>(
                 tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor,
-                nd, s_whist, s_keys, s_vals, s_gbase, s_wsum);
+                nd, s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum);
+        }
         __syncthreads();
+        cur ^= 1;
     }
     // hand the next slot's digit counts to global memory once per CTA
     if (nd.on && tid < kRadix && s_nhist[tid])
@@ -599,22 +681,25 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
 }
 
 // smallest tile over all configurations: sizes the look-back scratch
-constexpr int kMinTile = 256 * 12;
+constexpr int kMinTile = 512 * 6;
 
 template <typename U, bool VALS, typename LB>
 b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
     const int cfg = onesweep_cfg();
-    if constexpr (sizeof(U) == 4 && VALS) {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
+    if constexpr (sizeof(U) == 4 && VALS) {  // 8 B/pair in flight per item
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 3>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
         if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
+    } else if constexpr (VALS) {
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 3>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);
     } else {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 4>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
     }
 }
 
