@@ -20,6 +20,14 @@ $(LIB)/libb200sort.so: $(OBJS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
+# phase-profiling variant (clock64 per onesweep phase; tools/phase_prof.py)
+prof: $(LIB)/libb200sort_prof.so
+
+$(LIB)/libb200sort_prof.so: $(SRC)/*.cu $(HDRS)
+	@mkdir -p $(LIB) build/prof
+	for f in $(CU); do $(NVCC) $(NVFLAGS) -DB2S_PHASE_PROFILE -c $(SRC)/$$f.cu -o build/prof/$$f.o || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $@ $(addprefix build/prof/,$(addsuffix .o,$(CU))) -lcudart
+
 oracle:
 	bash oracle/build_ref.sh
 

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libb200sort.so")
+LIB_PATH = os.environ.get("B2S_LIB") or os.path.join(HERE, "lib", "libb200sort.so")
 
 B2S_OK, B2S_EINVAL, B2S_ENOMEM, B2S_ECUDA, B2S_EINTERNAL = range(5)
 B2S_I32, B2S_U32, B2S_I64, B2S_U64 = range(4)

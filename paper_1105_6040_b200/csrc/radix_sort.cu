@@ -37,6 +37,22 @@
 
 #include "b2s_internal.cuh"
 
+#ifdef B2S_PHASE_PROFILE
+// Debug build only (make prof): per-phase SM cycles of the onesweep kernel,
+// summed over CTAs, for thread 0 (a look-back warp) and the last thread.
+__device__ unsigned long long b2s_phase_cycles[2][8];
+#define B2S_PHASE(k)                                                   \
+    do {                                                               \
+        const long long t_ = clock64();                                \
+        prof_acc[k] += (unsigned long long)(t_ - prof_t);              \
+        prof_t = t_;                                                   \
+    } while (0)
+#else
+#define B2S_PHASE(k) \
+    do {             \
+    } while (0)
+#endif
+
 namespace b2s {
 namespace {
 
@@ -47,12 +63,14 @@ struct LookbackWord;
 template <>
 struct LookbackWord<uint32_t> {
     static constexpr uint32_t kAgg = 1u << 30, kInc = 2u << 30, kMask = (1u << 30) - 1;
+    static constexpr int kPrefetch = 4;
     static __device__ __forceinline__ uint32_t flag(uint32_t w) { return w >> 30; }
 };
 template <>
 struct LookbackWord<unsigned long long> {
     static constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62,
                                         kMask = (1ull << 62) - 1;
+    static constexpr int kPrefetch = 4;
     static __device__ __forceinline__ unsigned long long flag(unsigned long long w) {
         return w >> 62;
     }
@@ -275,6 +293,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void cp_async_lb(uint32_t dst, const uint32_t* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_lb(uint32_t dst, const unsigned long long* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -334,8 +358,9 @@ struct NextDigit {
 // One tile: keys come from `kbuf` (already landed by TMA) when FROM_SMEM,
 // else straight from global memory; the tile is then ranked, staged
 // digit-sorted back into `kbuf`/`vbuf`, and written out.
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM>
-__device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid, uint64_t tile_base,
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
+          int MATCH, typename Claim>
+__device__ __forceinline__ void onesweep_tile(const Claim& claim_next,uint32_t tile, uint32_t tile_valid, uint64_t tile_base,
                                               const U* __restrict__ src, U* __restrict__ dst,
                                               const uint32_t* __restrict__ vsrc,
                                               uint32_t* __restrict__ vdst,
@@ -343,11 +368,15 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
                                               LB* __restrict__ lb_cur, int shift, uint32_t dxor,
                                               const NextDigit nd, uint32_t* s_whist, U* kbuf,
                                               uint32_t* vbuf, unsigned long long* s_gbase,
-                                              uint32_t* s_wsum) {
+                                              uint32_t* s_wsum, LB* s_lbw,
+                                              unsigned long long* prof_acc, long long& prof_t) {
+    (void)prof_acc;
+    (void)prof_t;
     using W = LookbackWord<LB>;
     constexpr int WARPS = THREADS / 32;
     constexpr int WSEG = 32 * ITEMS;
-    constexpr int LOOKBACK = 4;  // predecessors read per look-back step
+    constexpr int LOOKBACK = 4;  // predecessors read per synchronous look-back step
+    constexpr int PRE = LookbackWord<LB>::kPrefetch;  // predecessors prefetched
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
@@ -392,6 +421,7 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
         else if (wbase + j * 32 + lane < tile_valid) red_add_shared(a, 1u);
     }
     __syncthreads();  // also: every warp has read its keys out of kbuf
+    B2S_PHASE(1);
 
     // ---- per digit: exclusive prefix over warps, tile count, publish early
     uint32_t count = 0, start = 0;
@@ -412,6 +442,19 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
         if (lane == 31) s_wsum[warp] = incl;
         start = incl - count;
     }
+    // start the look-back's first reads now (cp.async into shared memory, so
+    // no registers are held) so their latency hides behind the ranking below.
+    // A stale copy is harmless: a slot only moves 0 -> aggregate -> inclusive
+    // and every non-zero state is valid; zeros are re-polled.
+    if (tid < kRadix && tile > 0) {
+#pragma unroll
+        for (int i = 0; i < PRE; ++i) {
+            if ((int64_t)tile - 1 - i >= 0)
+                cp_async_lb(smem_addr(s_lbw + i * kRadix + tid),
+                            lb_cur + (size_t)(tile - 1 - i) * kRadix + tid);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     __syncthreads();
     if (tid < kRadix) {
 #pragma unroll
@@ -421,6 +464,7 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
     }
     __syncthreads();
 
+    B2S_PHASE(2);
     // ---- rank within the tile and stage digit-sorted in shared memory. The
     // warp's counters start at its offset for each digit; item j of lane l
     // precedes item j of lane l+1 and item j+1 of any lane (input order), so
@@ -432,7 +476,11 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
     for (int j = 0; j < ITEMS; ++j) {
         const bool valid = FULL || (wbase + j * 32 + lane < tile_valid);
         const uint32_t d = valid ? digit_of(keys[j], shift, dxor) : (uint32_t)kRadix;
-        const uint32_t peers = match_digit<FULL ? 8 : 9>(d);
+        uint32_t peers;
+        if (MATCH == 2 || (MATCH == 1 && (j & 1)))
+            peers = __match_any_sync(0xffffffffu, d);  // ADU pipe
+        else
+            peers = match_digit<FULL ? 8 : 9>(d);      // ALU pipe
         const uint32_t below = __popc(peers & lanemask_lt);
         const bool leader = (peers >> lane) == 1u;
         const uint32_t ca = wh_a + 4 * (d & (kRadix - 1));
@@ -444,21 +492,52 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
         }
     }
 
-    // ---- decoupled look-back: one lane per digit, LOOKBACK predecessors per
-    // step (independent loads), warp-uniform loop
+    // claim the next tile and start streaming it in now: late enough that
+    // claim order stays close to processing order (look-back predecessors are
+    // rarely still unpublished), early enough that the copy overlaps this
+    // tile's look-back and write-out
+    B2S_PHASE(3);
+    claim_next();
+
+    // ---- decoupled look-back: one lane per digit. The first PRE predecessors
+    // were fetched before ranking; later steps read LOOKBACK at a time
+    // (independent loads) in a warp-uniform loop.
     if (tid < kRadix) {
         unsigned long long excl = 0;
         if (tile > 0) {
             int64_t pred = (int64_t)tile - 1;
             bool done = false;
             const LB* col = lb_cur + tid;
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            bool stop = false;
+#pragma unroll
+            for (int i = 0; i < PRE; ++i) {
+                if (!stop) {
+                    const LB w = ((int64_t)tile - 1 - i >= 0) ? s_lbw[i * kRadix + tid] : W::kInc;
+                    const LB f = W::flag(w);
+                    if (f != 0) {
+                        excl += (unsigned long long)(w & W::kMask);
+                        done = (f == 2);
+                        stop = done;
+                        pred -= done ? 0 : 1;
+                    } else {
+                        stop = true;
+                    }
+                }
+            }
+#ifdef B2S_PHASE_PROFILE
+            if (tid == 0) prof_acc[7] += 1;  // look-back steps of digit 0
+#endif
             while (__any_sync(0xffffffffu, !done)) {
                 if (!done) {
+#ifdef B2S_PHASE_PROFILE
+                    if (tid == 0) prof_acc[7] += 1;
+#endif
                     LB w[LOOKBACK];
 #pragma unroll
                     for (int i = 0; i < LOOKBACK; ++i)
                         w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * kRadix) : W::kInc;
-                    bool stop = false;
+                    stop = false;
 #pragma unroll
                     for (int i = 0; i < LOOKBACK; ++i) {
                         const LB f = W::flag(w[i]);
@@ -479,6 +558,7 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
     }
     __syncthreads();
 
+    B2S_PHASE(4);
     // ---- write runs of equal digits: consecutive threads, consecutive slots;
     // count the next slot's digit on the way out; clear this warp's counters
 #pragma unroll
@@ -496,7 +576,7 @@ __device__ __forceinline__ void onesweep_tile(uint32_t tile, uint32_t tile_valid
     }
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int MATCH>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __restrict__ plan,
                                                                  RadixCounters* __restrict__ ctr,
                                                                  int slot, uint64_t n,
@@ -523,6 +603,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     __shared__ uint32_t s_wsum[kRadix / 32];
     __shared__ uint32_t s_tile[2];
     __shared__ alignas(8) unsigned long long s_mbar[2];
+    __shared__ alignas(16) LB s_lbw[LookbackWord<LB>::kPrefetch * kRadix];
 
     const int tid = threadIdx.x;
     const int shift = 8 * plan->digit[slot];
@@ -567,7 +648,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         s_nhist[tid] = 0;
     }
     for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_whist[i] = 0;
-    if (tid == 0) {
+    if (tid == THREADS - 1) {
         mbar_init(mbar_a[0], 1);
         mbar_init(mbar_a[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -585,37 +666,51 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
 
     int cur = 0;
     uint32_t parity = 0;  // bit b: phase parity of buffer b's mbarrier
+    unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_t = clock64();
     for (;;) {
         const uint32_t tile = s_tile[cur];
         if (tile >= ntiles) break;
-        if (tid == 0) {  // claim the next tile and start streaming it in
-            const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-            s_tile[cur ^ 1] = t;
-            prefetch(t, cur ^ 1);
-        }
+        auto claim = [&]() {  // by a thread that sits out the look-back
+            if (tid == THREADS - 1) {
+                const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
+                s_tile[cur ^ 1] = t;
+                prefetch(t, cur ^ 1);
+            }
+        };
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
         if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
         if (rem >= (uint64_t)TILE) {
             if (tma) {
+                B2S_PHASE(6);
                 mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
                 parity ^= 1u << cur;
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true>(
+                B2S_PHASE(0);
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, MATCH>(
+                    claim,
                     tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
-                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum);
+                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum, s_lbw, prof_acc, prof_t);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, MATCH>(
+                    claim,
                     tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
-                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum);
+                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum, s_lbw, prof_acc, prof_t);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, MATCH>(
+                claim,
                 tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor,
-                nd, s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum);
+                nd, s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum, s_lbw, prof_acc, prof_t);
         }
         __syncthreads();
+        B2S_PHASE(5);
         cur ^= 1;
     }
+#ifdef B2S_PHASE_PROFILE
+    if (tid == 0 || tid == THREADS - 1)
+        for (int k = 0; k < 8; ++k) atomicAdd(&b2s_phase_cycles[tid == 0 ? 0 : 1][k], prof_acc[k]);
+#endif
     // hand the next slot's digit counts to global memory once per CTA
     if (nd.on && tid < kRadix && s_nhist[tid])
         atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)s_nhist[tid]);
@@ -651,12 +746,12 @@ int onesweep_cfg() {
     return cfg;
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int MATCH = 0>
 b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
                              void* lb) {
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
-    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB>;
+    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, MATCH>;
     static int occ = -1;  // per instantiation, per process (single device type)
     if (occ < 0) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -693,6 +788,9 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
         if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 4) return launch_passes_cfg<U, VALS, LB, 512, 16, 2, 1>(ctx, plan, ctr, n, lb);
+        if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 16, 2, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 6) return launch_passes_cfg<U, VALS, LB, 256, 16, 4, 1>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 3>(ctx, plan, ctr, n, lb);
@@ -762,6 +860,17 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
 }
 
 }  // namespace
+
+#ifdef B2S_PHASE_PROFILE
+extern "C" int b2s_debug_phase_cycles(unsigned long long* out16, int reset) {
+    cudaMemcpyFromSymbol(out16, b2s_phase_cycles, sizeof(b2s_phase_cycles));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(b2s_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout,
                       const uint32_t* vin, uint32_t* vout, uint64_t n) {

@@ -1,0 +1,32 @@
+"""Per-phase cycle split of the onesweep kernel (debug library from `make prof`).
+
+  B2S_LIB=paper_1105_6040_b200/lib/libb200sort_prof.so python tools/phase_prof.py
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1105_6040_b200 import _lib  # noqa: E402
+from paper_1105_6040_b200.device import Context  # noqa: E402
+
+NAMES = ["tma_wait", "load+early_counts+sync", "digit_scan+sync", "rank", "lookback+sync",
+         "writeout+sync", "loop_top", "-"]
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 28
+ctx = Context(0)
+keys = ctx.gen_keys(n, 1, torch.uint32, shift=32)
+out = torch.empty_like(keys)
+ctx.sort(keys, out=out)
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 16)()
+_lib.lib().b2s_debug_phase_cycles(buf, 1)
+ctx.sort(keys, out=out)
+torch.cuda.synchronize()
+_lib.lib().b2s_debug_phase_cycles(buf, 1)
+tiles = (n + 8191) // 8192
+print(f"look-back steps per tile (digit 0): {buf[7] / (tiles * 4):.2f}")
+for who, off in (("thread 0 (look-back warp)", 0), ("last thread", 8)):
+    tot = sum(buf[off + k] for k in range(8)) or 1
+    print(who + ": " + ", ".join(f"{NAMES[k]} {100 * buf[off + k] / tot:.1f}%" for k in range(7)))
