@@ -44,6 +44,21 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _traffic(n):
+    """DRAM bytes per onesweep launch from the committed ncu --set full capture
+    (profiles/*_onesweep_traffic.json, newest round), when it matches n."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_onesweep_traffic.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f))
+            if d.get("algorithmic_bytes_per_launch") == 8 * n:
+                return d["traffic_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -240,7 +255,7 @@ def run_single(args):
                    "n": n, "p": 1, "key_bytes": 4,
                    "l2": "inputs (1 GiB) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": _traffic(n),
                      "kernel": "onesweep_kernel (one digit pass)",
                      "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": alg_bytes,

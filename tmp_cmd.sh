@@ -1,2 +1,5 @@
-for c in 0 1 3; do echo "cfg $c"; B2S_ONESWEEP_CFG=$c timeout 120 python tools/prof_sort.py --n 268435456 --iters 3 2>&1 | tail -1; done > gpurun_out/run.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_sort.py -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/run.log
+set -x
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench=$?
+python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
+ncu --set full --clock-control none --import-source on -k regex:onesweep -s 8 -c 1 -o gpurun_out/bench_onesweep python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
