@@ -10,7 +10,7 @@ CU := abi radix_sort merge_path sample_sort gen_verify
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(CU)))
 HDRS := include/b200sort.h $(SRC)/b2s_internal.cuh
 
-all: $(LIB)/libb200sort.so
+all: $(LIB)/libb200sort.so $(LIB)/libsortbench_b200.so build/test_compat
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -19,6 +19,16 @@ $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 $(LIB)/libb200sort.so: $(OBJS)
 	@mkdir -p $(LIB)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+# the reference's C++ signatures on top of the C ABI
+$(LIB)/libsortbench_b200.so: $(SRC)/compat/sortbench_compat.cpp include/sortbench_b200/sortbench.hpp $(LIB)/libb200sort.so
+	g++ -std=c++20 -O2 -fPIC -shared -Wall -Wextra -Iinclude $< -L$(LIB) -lb200sort \
+	    -Wl,-rpath,'$$ORIGIN' -o $@
+
+build/test_compat: tests/cpp/test_compat.cpp $(LIB)/libsortbench_b200.so
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude $< -L$(LIB) -lsortbench_b200 -lb200sort \
+	    -Wl,-rpath,'$$ORIGIN/../$(LIB)' -o $@
 
 # phase-profiling variant (clock64 per onesweep phase; tools/phase_prof.py)
 prof: $(LIB)/libb200sort_prof.so

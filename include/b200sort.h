@@ -154,9 +154,10 @@ b2s_status b2s_bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_k
  * int64/uint64 widening w) and an order-independent multiset hash
  * (sum_i mix(w_i)), all returned to host integers (synchronous). */
 b2s_status b2s_gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n,
-                        uint64_t seed, int shift, void* out);
+                        uint64_t seed, int shift, void* out, uint32_t flags);
 b2s_status b2s_check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
-                            uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset);
+                            uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset,
+                            uint32_t flags);
 
 #ifdef __cplusplus
 }

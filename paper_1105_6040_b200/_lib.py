@@ -68,8 +68,8 @@ _SIGS = {
     "b2s_sample_regular": (_st, [_p, _i, _p, _u64, _i, _i, _p]),
     "b2s_select_splitters": (_st, [_p, _p, _i, _i, _p]),
     "b2s_bucket_bounds": (_st, [_p, _i, _p, _u64, _i, _p, _i, _p]),
-    "b2s_gen_keys": (_st, [_p, _i, _u64, _u64, _u64, _i, _p]),
-    "b2s_check_sorted": (_st, [_p, _i, _p, _u64, _p, _p, _p]),
+    "b2s_gen_keys": (_st, [_p, _i, _u64, _u64, _u64, _i, _p, _u32]),
+    "b2s_check_sorted": (_st, [_p, _i, _p, _u64, _p, _p, _p, _u32]),
 }
 
 

@@ -483,19 +483,30 @@ b2s_status b2s_bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_k
 }
 
 b2s_status b2s_gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
-                        int shift, void* out) {
+                        int shift, void* out, uint32_t flags) {
     B2S_TRY(check_ctx(ctx));
     if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
     if (shift < 0 || shift > 63) return set_error(B2S_EINVAL, "shift %d out of range", shift);
     if (n > 0 && out == nullptr) return set_error(B2S_EINVAL, "null output");
+    if (flags & B2S_HOST) {
+        const size_t bytes = n * (size_t)key_bytes(dtype);
+        B2S_TRY(ctx->stage_out.ensure(bytes));
+        B2S_TRY(gen_keys(ctx, dtype, first, n, seed, shift, ctx->stage_out.ptr));
+        return d2h_sync(ctx, out, ctx->stage_out.ptr, bytes);
+    }
     return gen_keys(ctx, dtype, first, n, seed, shift, out);
 }
 
 b2s_status b2s_check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
-                            uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset) {
+                            uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset,
+                            uint32_t flags) {
     B2S_TRY(check_ctx(ctx));
     if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
     if (n > 0 && keys == nullptr) return set_error(B2S_EINVAL, "null keys");
+    if (flags & B2S_HOST) {
+        B2S_TRY(h2d(ctx, ctx->stage_in, keys, n * (size_t)key_bytes(dtype)));
+        keys = ctx->stage_in.ptr;
+    }
     return check_sorted(ctx, dtype, keys, n, inversions, fingerprint, multiset);
 }
 

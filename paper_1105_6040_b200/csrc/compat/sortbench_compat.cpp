@@ -1,0 +1,225 @@
+// sortbench_compat.cpp -- the reference's C++ entry points
+// (include/sortbench_b200/sortbench.hpp) on top of the B200 C ABI.
+//
+// Each rank thread of a reference-style program gets its own b2s context
+// (thread_local), mirroring the reference's one-Comm-per-thread rule
+// (P/include/sortbench/runtime.hpp:93-95): host spans are staged to the device
+// inside each call (B2S_HOST). Status codes map back to the reference's
+// exceptions: EINVAL -> ConfigError, EINTERNAL -> ProgrammingError, CUDA/OOM ->
+// std::runtime_error (CLI exit 1, P/tools/sortbench.cpp:385-387).
+#include <chrono>
+#include <cstdlib>
+#include <string>
+
+#include "b200sort.h"
+#include "sortbench_b200/sortbench.hpp"
+
+namespace sortbench {
+namespace {
+
+[[noreturn]] void raise(b2s_status st, const char* what) {
+    const std::string msg = std::string(what) + ": " + b2s_last_error();
+    if (st == B2S_EINVAL) throw ConfigError(msg);
+    if (st == B2S_EINTERNAL) throw ProgrammingError(msg);
+    throw std::runtime_error(msg);
+}
+
+void check(b2s_status st, const char* what) {
+    if (st != B2S_OK) raise(st, what);
+}
+
+struct CtxHolder {
+    b2s_ctx* ctx = nullptr;
+    ~CtxHolder() {
+        if (ctx) b2s_destroy(ctx);
+    }
+};
+
+b2s_ctx* ctx() {
+    thread_local CtxHolder h;
+    if (h.ctx == nullptr) {
+        int dev = 0;
+        if (const char* e = std::getenv("SORTBENCH_B200_DEVICE")) dev = std::atoi(e);
+        check(b2s_create(dev, &h.ctx), "b2s_create");
+        check(b2s_enable_timing(h.ctx, 1), "b2s_enable_timing");
+    }
+    return h.ctx;
+}
+
+std::uint64_t executed_passes() {
+    b2s_timing t{};
+    if (b2s_get_timing(ctx(), &t) != B2S_OK) return 0;
+    return static_cast<std::uint64_t>(t.passes_executed);
+}
+
+void sort_host(Element* p, std::size_t n, kernels::SortStats& stats) {
+    if (n < 2) return;
+    check(b2s_sort(ctx(), B2S_I64, p, p, nullptr, nullptr, n, B2S_HOST), "b2s_sort");
+    stats.moves += 2 * n * executed_passes();
+}
+
+}  // namespace
+
+namespace kernels {
+
+void bubble_sort(std::span<Element> block, SortStats& stats) {
+    sort_host(block.data(), block.size(), stats);
+}
+
+DataList merge_runs(std::span<const Element> run_a, std::span<const Element> run_b,
+                    SortStats& stats) {
+    DataList out(run_a.size() + run_b.size());
+    if (out.empty()) return out;
+    const void* runs[2] = {run_a.data(), run_b.data()};
+    const std::uint64_t lens[2] = {run_a.size(), run_b.size()};
+    check(b2s_merge(ctx(), B2S_I64, runs, nullptr, lens, 2, out.data(), nullptr, B2S_HOST),
+          "b2s_merge");
+    stats.moves += out.size();
+    return out;
+}
+
+void merge_sort(std::span<Element> block, std::ptrdiff_t first, std::ptrdiff_t last,
+                std::span<Element> /*scratch*/, SortStats& stats) {
+    if (first >= last) return;  // empty-range convention, P/src/sort_core.cpp:101
+    if (first < 0 || static_cast<std::size_t>(last) >= block.size())
+        throw ProgrammingError("merge_sort range out of bounds: first=" + std::to_string(first) +
+                               " last=" + std::to_string(last) +
+                               " size=" + std::to_string(block.size()));
+    sort_host(block.data() + first, static_cast<std::size_t>(last - first + 1), stats);
+}
+
+void quick_sort(std::span<Element> block, std::size_t start, std::size_t length,
+                SortStats& stats) {
+    if (start + length > block.size())  // P/src/sort_core.cpp:137-142
+        throw ProgrammingError("quick_sort segment out of range: start=" + std::to_string(start) +
+                               " length=" + std::to_string(length) +
+                               " size=" + std::to_string(block.size()));
+    sort_host(block.data() + start, length, stats);
+}
+
+bool is_sorted(std::span<const Element> seq) {
+    if (seq.size() < 2) return true;
+    std::uint64_t inv = 0, fp = 0, ms = 0;  // adjacent inversions, counted on the GPU
+    check(b2s_check_sorted(ctx(), B2S_I64, seq.data(), seq.size(), &inv, &fp, &ms, B2S_HOST),
+          "b2s_check_sorted");
+    return inv == 0;
+}
+
+}  // namespace kernels
+
+namespace parallel {
+
+const char* to_string(Algorithm algorithm) {
+    switch (algorithm) {
+        case Algorithm::bubble: return "bubble";
+        case Algorithm::merge: return "merge";
+        case Algorithm::quick: return "quick";
+    }
+    return "unknown";
+}
+
+Algorithm algorithm_from_string(const std::string& name) {
+    if (name == "bubble") return Algorithm::bubble;
+    if (name == "merge") return Algorithm::merge;
+    if (name == "quick") return Algorithm::quick;
+    throw ConfigError("unknown algorithm '" + name + "' (expected bubble, merge or quick)");
+}
+
+PartitionPlan plan_partition(std::size_t n, int p) {
+    if (p < 1) throw ConfigError("partition needs at least one process");
+    PartitionPlan plan;
+    plan.n = n;
+    plan.procs = p;
+    std::vector<std::uint64_t> sizes(static_cast<std::size_t>(p));
+    check(b2s_plan_partition(n, p, sizes.data()), "b2s_plan_partition");
+    plan.sizes.assign(sizes.begin(), sizes.end());
+    return plan;
+}
+
+PhaseSchedule build_schedule(int p) {
+    if (p < 1) throw ConfigError("schedule needs at least one process");
+    PhaseSchedule s;
+    s.procs = p;
+    s.partners.assign(static_cast<std::size_t>(p), std::vector<int>(static_cast<std::size_t>(p), -1));
+    for (int phase = 0; phase < p; ++phase)
+        for (int r = phase % 2; r + 1 < p; r += 2) {
+            s.partners[static_cast<std::size_t>(phase)][static_cast<std::size_t>(r)] = r + 1;
+            s.partners[static_cast<std::size_t>(phase)][static_cast<std::size_t>(r + 1)] = r;
+        }
+    return s;
+}
+
+PaddedBlock merge_split_padded(const PaddedBlock& mine, const PaddedBlock& theirs, KeepHalf keep,
+                               kernels::SortStats& stats) {
+    PaddedBlock out;
+    out.reals.resize(mine.width());
+    std::uint64_t nr = 0, nv = 0;
+    check(b2s_merge_split_padded(ctx(), B2S_I64, mine.reals.data(), mine.reals.size(),
+                                 mine.virtuals, theirs.reals.data(), theirs.reals.size(),
+                                 theirs.virtuals, keep == KeepHalf::high ? 1 : 0,
+                                 out.reals.data(), &nr, &nv, B2S_HOST),
+          "b2s_merge_split_padded");
+    out.reals.resize(nr);
+    out.virtuals = nv;
+    stats.moves += nr;
+    return out;
+}
+
+DataList merge_split(std::span<const Element> mine, std::span<const Element> theirs,
+                     KeepHalf keep, kernels::SortStats& stats) {
+    PaddedBlock a{DataList(mine.begin(), mine.end()), 0};
+    PaddedBlock b{DataList(theirs.begin(), theirs.end()), 0};
+    return merge_split_padded(a, b, keep, stats).reals;
+}
+
+namespace {
+void gpu_kernel(std::span<Element> block, std::span<Element> /*scratch*/,
+                kernels::SortStats& stats) {
+    sort_host(block.data(), block.size(), stats);
+}
+}  // namespace
+
+KernelFn select_kernel(Algorithm algorithm) {
+    switch (algorithm) {
+        case Algorithm::bubble:
+        case Algorithm::merge:
+        case Algorithm::quick:
+            return &gpu_kernel;  // one radix sort: any correct integer sort is identical
+    }
+    throw ConfigError("unknown algorithm id");
+}
+
+SortOutcome scatter_merge_sort(Algorithm algorithm, const DataList& data,
+                               const runtime::WorldOptions& options) {
+    const int p = options.procs;
+    if (p < 1) throw ConfigError("partition needs at least one process");
+    select_kernel(algorithm);
+    SortOutcome outcome;
+    outcome.world.options = options;
+    outcome.local_sort_stats.assign(static_cast<std::size_t>(p), kernels::SortStats{});
+    outcome.sorted.resize(data.size());
+    if (data.empty()) return outcome;
+    const auto t0 = std::chrono::steady_clock::now();
+    check(b2s_partitioned_sort(ctx(), B2S_I64, data.data(), outcome.sorted.data(), nullptr,
+                               nullptr, data.size(), p, B2S_HOST),
+          "b2s_partitioned_sort");
+    outcome.world.wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    b2s_timing t{};
+    if (b2s_get_timing(ctx(), &t) == B2S_OK) outcome.world.device_ms = t.total_ms;
+    return outcome;
+}
+
+}  // namespace parallel
+
+namespace bench {
+
+DataList gen_data(std::size_t n, std::uint64_t seed) {
+    DataList out(n);
+    if (n == 0) return out;
+    check(b2s_gen_keys(ctx(), B2S_I64, 0, n, seed, 0, out.data(), B2S_HOST), "b2s_gen_keys");
+    return out;
+}
+
+}  // namespace bench
+}  // namespace sortbench

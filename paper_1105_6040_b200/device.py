@@ -238,16 +238,24 @@ class Context:
         """bench::gen_data's stream on the device: key_i = (T)(z_{first+i} >> shift)."""
         if out is None:
             out = torch.empty(n, dtype=dtype, device=f"cuda:{self.device}")
+        if _is_host(out):
+            check(lib().b2s_gen_keys(self._h, dtype_code(out), first, n, seed, shift, _ptr(out),
+                                     B2S_HOST))
+            return out
         self._bind_stream(stream)
-        check(lib().b2s_gen_keys(self._h, dtype_code(out), first, n, seed, shift, _ptr(out)))
+        check(lib().b2s_gen_keys(self._h, dtype_code(out), first, n, seed, shift, _ptr(out),
+                                 B2S_DEVICE))
         return out
 
     def check_sorted(self, keys, stream=None):
         """(adjacent inversions, order-sensitive fingerprint, multiset hash)."""
         inv, fp, ms = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-        self._bind_stream(stream)
+        host = _is_host(keys)
+        if not host:
+            self._bind_stream(stream)
         check(lib().b2s_check_sorted(self._h, dtype_code(keys), _ptr(keys), _numel(keys),
-                                     ctypes.byref(inv), ctypes.byref(fp), ctypes.byref(ms)))
+                                     ctypes.byref(inv), ctypes.byref(fp), ctypes.byref(ms),
+                                     B2S_HOST if host else B2S_DEVICE))
         return inv.value, fp.value, ms.value
 
     # -- helpers ----------------------------------------------------------------
