@@ -159,7 +159,7 @@ b2s_status merge2_window(b2s_ctx* ctx, const T* a, const uint32_t* va, uint64_t 
     merge_partition_window_kernel<T><<<(unsigned)((np + 255) / 256), 256, 0, ctx->stream>>>(
         a, na, b, nb, lo, hi, TILE, np, parts);
     B2S_LAUNCHED();
-    if (va != nullptr)
+    if (vout != nullptr)  // a run may be empty (null values) while the output has a payload
         merge_tile_kernel<T, true><<<(unsigned)ntiles, kMergeThreads, 0, ctx->stream>>>(
             a, va, na, b, vb, nb, parts, lo, hi, out, vout);
     else

@@ -100,3 +100,15 @@ def test_partitioned_sort_pairs_stable(ctx):
     for p in (1, 3, 4, 8):
         ok, ov = ctx.partitioned_sort(keys, p, vals=vals)
         assert np.array_equal(ok, ek) and np.array_equal(ov, ev), p
+
+
+def test_merge_empty_runs_with_payload(ctx):
+    """Regression: an empty run carries a null payload pointer; the payload of
+    the other runs must still be merged."""
+    k = torch.full((5000,), 7, dtype=torch.int32, device="cuda")
+    v = torch.arange(5000, dtype=torch.int32, device="cuda")
+    e, ev = k[:0], v[:0]
+    for runs, vals in (([e, k], [ev, v]), ([k, e], [v, ev]), ([e, k, e, k], [ev, v, ev, v])):
+        ok, ov = ctx.merge(runs, vals=vals)
+        torch.cuda.synchronize()
+        assert torch.equal(ov, torch.cat([x for x in vals]))
