@@ -95,7 +95,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 
 template <typename U>
 __device__ __forceinline__ uint32_t digit_of(U k, int shift, uint32_t dxor) {
-    return ((uint32_t)(k >> shift) & 0xFFu) ^ dxor;
+    // digits are whole bytes: one byte-permute extracts one (PRMT) instead of
+    // a shift and a mask on the saturated ALU pipe
+    uint32_t w;
+    if constexpr (sizeof(U) == 4) w = (uint32_t)k;
+    else w = shift >= 32 ? (uint32_t)((unsigned long long)k >> 32) : (uint32_t)k;
+    return __byte_perm(w, 0u, 0x4440u | ((shift >> 3) & 3)) ^ dxor;
 }
 
 // ---------------------------------------------------------------------------
@@ -257,17 +262,29 @@ __global__ void __launch_bounds__(512) radix_fallback_hist_kernel(const RadixPla
 
 // ---------------------------------------------------------------------------
 // onesweep digit pass
+#ifndef B2S_MATCH_HYBRID
+#define B2S_MATCH_HYBRID 2
+#endif
+constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
+//
+// Shared-memory traffic is this kernel's bound on B200 (HBM is 6.5 TB/s but
+// the random-access shared memory work per key is ~15-20 wavefronts per 32
+// keys), so the layout minimises wavefronts: per-warp digit counters are
+// packed two 16-bit counters per word (a warp-tile count is <= 8192), ranks
+// are claimed by one shared atomic per digit group (the group's highest lane)
+// and broadcast with a shuffle, and global offsets are 32-bit when n < 2^30.
 
 template <typename U, bool VALS, int THREADS, int ITEMS>
 struct OnesweepSmem {
     static constexpr int WARPS = THREADS / 32;
     static constexpr int TILE = THREADS * ITEMS;
-    static constexpr size_t kWhist = (size_t)WARPS * kRadix * 4;
-    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);  // one tile buffer
+    static constexpr size_t kCnt = (size_t)WARPS * (kRadix / 2) * 4;  // packed u16 pairs
+    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);         // one tile buffer
     static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
-    // whist | keys[2] | vals[2]: tile i+1 streams in by TMA while tile i is
-    // ranked in place in its own buffer
-    static constexpr size_t bytes = kWhist + 2 * kKeys + 2 * kVals;
+    static constexpr size_t kMatch = MATCH_SMEM ? (size_t)WARPS * kRadix * 4 : 0;
+    // counters | keys[2] | vals[2] | match masks: tile i+1 streams in by TMA
+    // while tile i is ranked in place in its own buffer
+    static constexpr size_t bytes = kCnt + 2 * kKeys + 2 * kVals + kMatch;
 };
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier ----------
@@ -304,8 +321,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // Lanes of the warp whose digit equals mine, from one ballot per digit bit
-// (VOTE + logic ops only: MATCH.ANY and FLO serialise on the SM's shared
-// ADU/XU pipes, which capped the first version at ~1 TB/s).
+// (VOTE + logic ops only: MATCH.ANY serialises on the SM's shared ADU pipe).
 template <int BITS>
 __device__ __forceinline__ uint32_t match_digit(uint32_t d) {
     uint32_t peers = 0xffffffffu;
@@ -324,22 +340,45 @@ __device__ __forceinline__ uint32_t match_digit(uint32_t d) {
     return peers;
 }
 
-// 32-bit shared-window addressing: computed once, so the per-key shared
-// accesses below cost one address add instead of a generic->shared conversion.
+// Shared-memory match: every valid lane ORs its bit into its digit's mask,
+// reads the mask back (= its peers), and clears it. The warp is converged and
+// its shared accesses run in program order, so all ORs land before the reads
+// and all reads before the clears.
+__device__ __forceinline__ uint32_t match_smem(bool valid, uint32_t a, uint32_t bit) {
+    uint32_t peers;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.u32 q, %1, 0;\n\t"
+        "@q red.shared.or.b32 [%2], %3;\n\t"
+        "@q ld.volatile.shared.u32 %0, [%2];\n\t"
+        "@q st.volatile.shared.u32 [%2], 0;\n\t}"
+        : "=r"(peers)
+        : "r"((uint32_t)valid), "r"(a), "r"(bit)
+        : "memory");
+    return valid ? peers : 0u;
+}
+
+// 32-bit shared-window addressing, computed once per kernel
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts_u32_if(bool pred, uint32_t a, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.volatile.shared.u32 [%0], %1;\n\t}"
-                 ::"r"(a), "r"(v), "r"((uint32_t)pred) : "memory");
-}
 __device__ __forceinline__ void red_add_shared(uint32_t a, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+// predicated shared atomic add returning the old word (0 when !pred)
+__device__ __forceinline__ uint32_t atom_add_shared_if(bool pred, uint32_t a, uint32_t v) {
+    uint32_t old = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                 "@q atom.shared.add.u32 %0, [%1], %2;\n\t}"
+                 : "+r"(old)
+                 : "r"(a), "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+    return old;
 }
 __device__ __forceinline__ void sts_key(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -355,34 +394,55 @@ struct NextDigit {
     uint32_t hist_a;  // shared address of the next slot's digit counters
 };
 
-// One tile: keys come from `kbuf` (already landed by TMA) when FROM_SMEM,
-// else straight from global memory; the tile is then ranked, staged
-// digit-sorted back into `kbuf`/`vbuf`, and written out.
+// Shared state of one CTA besides the tile buffers.
+template <typename LB>
+struct TileShared {
+    using OFF = LB;  // 32-bit offsets exactly when the look-back words are 32-bit (n < 2^30)
+    OFF gbase[kRadix];   // this tile's global base per digit (minus its tile start)
+    OFF goff[kRadix];    // the slot's global digit offsets
+    uint32_t nhist[kRadix];
+    uint32_t start[kRadix];
+    uint32_t wsum[kRadix / 32];
+    unsigned long long wsum64[kRadix / 32];
+    alignas(16) LB lbw[4 * kRadix];  // prefetched look-back window
+    uint32_t tile[2];
+    uint32_t dummy[32];  // sink of the non-leaders' no-op rank atomics
+    alignas(8) unsigned long long mbar[2];
+};
+
+// One tile: keys come from `kbuf` (landed by TMA) when FROM_SMEM, else from
+// global memory; the tile is ranked, staged digit-sorted back into
+// `kbuf`/`vbuf`, and written out.
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
-          int MATCH, typename Claim>
-__device__ __forceinline__ void onesweep_tile(const Claim& claim_next,uint32_t tile, uint32_t tile_valid, uint64_t tile_base,
+          typename Claim>
+__device__ __forceinline__ void onesweep_tile(const Claim& claim_next, uint32_t tile,
+                                              uint32_t tile_valid, uint64_t tile_base,
                                               const U* __restrict__ src, U* __restrict__ dst,
                                               const uint32_t* __restrict__ vsrc,
-                                              uint32_t* __restrict__ vdst,
-                                              const unsigned long long* s_goff,
-                                              LB* __restrict__ lb_cur, int shift, uint32_t dxor,
-                                              const NextDigit nd, uint32_t* s_whist, U* kbuf,
-                                              uint32_t* vbuf, unsigned long long* s_gbase,
-                                              uint32_t* s_wsum, LB* s_lbw,
-                                              unsigned long long* prof_acc, long long& prof_t) {
+                                              uint32_t* __restrict__ vdst, LB* __restrict__ lb_cur,
+                                              int shift, uint32_t dxor, const NextDigit nd,
+                                              uint32_t* s_cnt, U* kbuf, uint32_t* vbuf,
+                                              uint32_t* s_match, TileShared<LB>& sh,
+                                              unsigned long long* prof_acc,
+                                              long long& prof_t) {
     (void)prof_acc;
     (void)prof_t;
     using W = LookbackWord<LB>;
+    using OFF = typename TileShared<LB>::OFF;
     constexpr int WARPS = THREADS / 32;
     constexpr int WSEG = 32 * ITEMS;
-    constexpr int LOOKBACK = 4;  // predecessors read per synchronous look-back step
-    constexpr int PRE = LookbackWord<LB>::kPrefetch;  // predecessors prefetched
+    constexpr int LOOKBACK = 4;   // predecessors read per synchronous look-back step
+    constexpr int PRE = 4;        // predecessors prefetched before ranking
+    constexpr int HALF = kRadix / 2;
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    const uint32_t wh_a = smem_addr(s_whist + warp * kRadix);
+    const uint32_t cnt_a = smem_addr(s_cnt + warp * HALF);
     const uint32_t keys_a = smem_addr(kbuf);
     const uint32_t vals_a = smem_addr(vbuf);
+    const uint32_t match_a = smem_addr(s_match + warp * kRadix);
+    (void)match_a;
+    const uint32_t dummy_a = smem_addr(sh.dummy + lane);
 
     // ---- load: warp w owns keys [w*WSEG, (w+1)*WSEG) of the tile; item j of
     // lane l is key j*32+l (coalesced / conflict-free; in-warp order == input order)
@@ -413,107 +473,135 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next,uint32_t t
         }
     }
 
-    // ---- early counts: per-warp digit histogram with shared reductions
+    // ---- early counts: per-warp digit histogram (packed 16-bit halves)
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t a = wh_a + 4 * digit_of(keys[j], shift, dxor);
-        if (FULL) red_add_shared(a, 1u);
-        else if (wbase + j * 32 + lane < tile_valid) red_add_shared(a, 1u);
+        const uint32_t d = digit_of(keys[j], shift, dxor);
+        const uint32_t a = cnt_a + 4 * (d >> 1);
+        if (FULL || wbase + j * 32 + lane < tile_valid) red_add_shared(a, 1u << (16 * (d & 1)));
     }
     __syncthreads();  // also: every warp has read its keys out of kbuf
     B2S_PHASE(1);
 
-    // ---- per digit: exclusive prefix over warps, tile count, publish early
-    uint32_t count = 0, start = 0;
-    if (tid < kRadix) {
+    // ---- per digit pair (thread t < 128 owns digits 2t, 2t+1): exclusive
+    // prefix over warps, tile counts, publish them at once
+    uint32_t pair = 0;  // packed tile counts of the two digits
+    if (tid < HALF) {
 #pragma unroll 4
         for (int w = 0; w < WARPS; ++w) {
-            const uint32_t c = s_whist[w * kRadix + tid];
-            s_whist[w * kRadix + tid] = count;
-            count += c;
+            const uint32_t c = s_cnt[w * HALF + tid];
+            s_cnt[w * HALF + tid] = pair;
+            pair += c;
         }
-        st_relaxed(lb_cur + (size_t)tile * kRadix + tid, (tile == 0 ? W::kInc : W::kAgg) | (LB)count);
-        uint32_t incl = count;
+        const uint32_t c0 = pair & 0xFFFFu, c1 = pair >> 16;
+        LB* slot = lb_cur + (size_t)tile * kRadix + 2 * tid;
+        const LB flag = tile == 0 ? W::kInc : W::kAgg;
+        st_relaxed(slot, flag | (LB)c0);
+        st_relaxed(slot + 1, flag | (LB)c1);
+        uint32_t incl = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (lane == 31) s_wsum[warp] = incl;
-        start = incl - count;
+        if (lane == 31) sh.wsum[warp] = incl;
+        sh.start[2 * tid] = incl - c0 - c1;  // partial (within warp)
+        sh.start[2 * tid + 1] = incl - c1;
     }
-    // start the look-back's first reads now (cp.async into shared memory, so
-    // no registers are held) so their latency hides behind the ranking below.
-    // A stale copy is harmless: a slot only moves 0 -> aggregate -> inclusive
-    // and every non-zero state is valid; zeros are re-polled.
+    // start the look-back's first reads now (cp.async into shared memory, no
+    // registers held) so their latency hides behind the ranking below. A stale
+    // copy is harmless: a slot only moves 0 -> aggregate -> inclusive and every
+    // non-zero state is valid; zeros are re-polled.
     if (tid < kRadix && tile > 0) {
 #pragma unroll
         for (int i = 0; i < PRE; ++i) {
             if ((int64_t)tile - 1 - i >= 0)
-                cp_async_lb(smem_addr(s_lbw + i * kRadix + tid),
+                cp_async_lb(smem_addr(sh.lbw + i * kRadix + tid),
                             lb_cur + (size_t)(tile - 1 - i) * kRadix + tid);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __syncthreads();
-    if (tid < kRadix) {
+    if (tid < HALF) {
+        uint32_t base = 0;
 #pragma unroll
-        for (int w = 0; w < kRadix / 32; ++w) start += (w < warp) ? s_wsum[w] : 0u;
+        for (int w = 0; w < HALF / 32; ++w) base += (w < warp) ? sh.wsum[w] : 0u;
+        const uint32_t s0 = sh.start[2 * tid] + base, s1 = sh.start[2 * tid + 1] + base;
+        sh.start[2 * tid] = s0;
+        sh.start[2 * tid + 1] = s1;
+        const uint32_t add = s0 | (s1 << 16);
 #pragma unroll 4
-        for (int w = 0; w < WARPS; ++w) s_whist[w * kRadix + tid] += start;
+        for (int w = 0; w < WARPS; ++w) s_cnt[w * HALF + tid] += add;
     }
     __syncthreads();
-
     B2S_PHASE(2);
+
     // ---- rank within the tile and stage digit-sorted in shared memory. The
     // warp's counters start at its offset for each digit; item j of lane l
     // precedes item j of lane l+1 and item j+1 of any lane (input order), so
-    // ranks are stable. The highest peer advances the counter. A warp's
-    // shared accesses are performed in program order and the loop has no
-    // divergent branch, so item j+1 reads item j's update without a barrier.
+    // ranks are stable. The highest lane of each digit group claims the group's
+    // slots with one atomic and shuffles the base to its peers.
     const uint32_t lanemask_lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const bool valid = FULL || (wbase + j * 32 + lane < tile_valid);
         const uint32_t d = valid ? digit_of(keys[j], shift, dxor) : (uint32_t)kRadix;
+#ifdef B2S_ABLATE_RANK
+        const uint32_t peers = 1u << lane;
+#else
         uint32_t peers;
-        if (MATCH == 2 || (MATCH == 1 && (j & 1)))
-            peers = __match_any_sync(0xffffffffu, d);  // ADU pipe
-        else
-            peers = match_digit<FULL ? 8 : 9>(d);      // ALU pipe
+        if (MATCH_SMEM && (B2S_MATCH_HYBRID == 1 || (j % B2S_MATCH_HYBRID) != 0)) {
+            // odd items: OR-mask match through shared memory (LSU pipe) to
+            // balance the ALU pipe the ballot match saturates
+            peers = match_smem(valid, match_a + 4 * (d & (kRadix - 1)), 1u << lane);
+        } else {
+            peers = match_digit<FULL ? 8 : 9>(d);
+        }
+#endif
         const uint32_t below = __popc(peers & lanemask_lt);
-        const bool leader = (peers >> lane) == 1u;
-        const uint32_t ca = wh_a + 4 * (d & (kRadix - 1));
-        const uint32_t r = lds_u32(ca) + below;
-        sts_u32_if(valid && leader, ca, r + 1);
+        const int leader = 31 - __clz(peers);
+        const uint32_t sh16 = 16 * (d & 1);
+        // every lane issues the atomic (no divergent branch: a branch costs two
+        // ADU-pipe reconvergence ops per item); non-leaders add 0 to a private
+        // dummy word so they neither conflict with nor change the counters
+        const bool claim = valid && lane == leader;
+        const uint32_t old = atom_add_shared(claim ? cnt_a + 4 * ((d >> 1) & (HALF - 1)) : dummy_a,
+                                             claim ? (below + 1) << sh16 : 0u);
+        const uint32_t base = (__shfl_sync(0xffffffffu, old, leader) >> sh16) & 0xFFFFu;
+        const uint32_t r = base + below;
+#ifdef B2S_ABLATE_SCATTER
+        if (valid && r == 0x7fffffff) {
+#else
         if (valid) {
+#endif
             sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j]);
             if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j]);
         }
     }
-
-    // claim the next tile and start streaming it in now: late enough that
-    // claim order stays close to processing order (look-back predecessors are
-    // rarely still unpublished), early enough that the copy overlaps this
-    // tile's look-back and write-out
     B2S_PHASE(3);
-    claim_next();
 
     // ---- decoupled look-back: one lane per digit. The first PRE predecessors
     // were fetched before ranking; later steps read LOOKBACK at a time
-    // (independent loads) in a warp-uniform loop.
+    // (independent loads) in a warp-uniform loop. Each lane publishes its
+    // inclusive prefix the moment it is known.
     if (tid < kRadix) {
         unsigned long long excl = 0;
+        const uint32_t mycount = (tid + 1 < kRadix ? sh.start[tid + 1] : (uint32_t)tile_valid) - sh.start[tid];
+#ifdef B2S_ABLATE_LOOKBACK
+        if (false) {
+#else
         if (tile > 0) {
+#endif
             int64_t pred = (int64_t)tile - 1;
             bool done = false;
             const LB* col = lb_cur + tid;
+            LB* mine = lb_cur + (size_t)tile * kRadix + tid;
             asm volatile("cp.async.wait_all;" ::: "memory");
             bool stop = false;
 #pragma unroll
             for (int i = 0; i < PRE; ++i) {
                 if (!stop) {
-                    const LB w = ((int64_t)tile - 1 - i >= 0) ? s_lbw[i * kRadix + tid] : W::kInc;
+                    const LB w = ((int64_t)tile - 1 - i >= 0) ? sh.lbw[i * kRadix + tid] : W::kInc;
                     const LB f = W::flag(w);
                     if (f != 0) {
                         excl += (unsigned long long)(w & W::kMask);
@@ -525,14 +613,12 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next,uint32_t t
                     }
                 }
             }
-#ifdef B2S_PHASE_PROFILE
-            if (tid == 0) prof_acc[7] += 1;  // look-back steps of digit 0
-#endif
+            if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
             while (__any_sync(0xffffffffu, !done)) {
-                if (!done) {
 #ifdef B2S_PHASE_PROFILE
-                    if (tid == 0) prof_acc[7] += 1;
+                if (tid == 0) prof_acc[7] += 1;
 #endif
+                if (!done) {
                     LB w[LOOKBACK];
 #pragma unroll
                     for (int i = 0; i < LOOKBACK; ++i)
@@ -550,33 +636,39 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next,uint32_t t
                             stop = true;
                         }
                     }
+                    if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
                 }
             }
-            st_relaxed(lb_cur + (size_t)tile * kRadix + tid, W::kInc | (LB)(excl + count));
         }
-        s_gbase[tid] = s_goff[tid] + excl - start;
+        sh.gbase[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
     }
     __syncthreads();
-
     B2S_PHASE(4);
+    claim_next();
+
     // ---- write runs of equal digits: consecutive threads, consecutive slots;
     // count the next slot's digit on the way out; clear this warp's counters
 #pragma unroll
-    for (int i = lane; i < kRadix; i += 32) s_whist[warp * kRadix + i] = 0;
+    for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t i = j * THREADS + tid;
         if (FULL || i < tile_valid) {
             const U k = kbuf[i];
-            const unsigned long long g = s_gbase[digit_of(k, shift, dxor)] + i;
+            const OFF g = sh.gbase[digit_of(k, shift, dxor)] + (OFF)i;
+#ifdef B2S_ABLATE_WRITE
+            if (k == (U)0x12345678 && g == 0)
+#endif
             __stcs(dst + g, k);
             if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
+#ifndef B2S_ABLATE_NEXTHIST
             if (nd.on) red_add_shared(nd.hist_a + 4 * digit_of(k, nd.shift, nd.dxor), 1u);
+#endif
         }
     }
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int MATCH>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __restrict__ plan,
                                                                  RadixCounters* __restrict__ ctr,
                                                                  int slot, uint64_t n,
@@ -586,24 +678,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
     static_assert(THREADS >= kRadix, "one thread per digit is required");
+    static_assert(TILE < 65536, "packed 16-bit warp counters");
 
     const int na = plan->num_active;
     if (slot >= na) return;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    uint32_t* s_whist = reinterpret_cast<uint32_t*>(smem);
-    U* kbuf[2] = {reinterpret_cast<U*>(smem + SM::kWhist),
-                  reinterpret_cast<U*>(smem + SM::kWhist + SM::kKeys)};
-    uint32_t* vbuf[2] = {reinterpret_cast<uint32_t*>(smem + SM::kWhist + 2 * SM::kKeys),
-                         reinterpret_cast<uint32_t*>(smem + SM::kWhist + 2 * SM::kKeys + SM::kVals)};
-    __shared__ unsigned long long s_gbase[kRadix];
-    __shared__ unsigned long long s_goff[kRadix];
-    __shared__ uint32_t s_nhist[kRadix];
-    __shared__ unsigned long long s_wsum64[kRadix / 32];
-    __shared__ uint32_t s_wsum[kRadix / 32];
-    __shared__ uint32_t s_tile[2];
-    __shared__ alignas(8) unsigned long long s_mbar[2];
-    __shared__ alignas(16) LB s_lbw[LookbackWord<LB>::kPrefetch * kRadix];
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);
+    U* kbuf[2] = {reinterpret_cast<U*>(smem + SM::kCnt),
+                  reinterpret_cast<U*>(smem + SM::kCnt + SM::kKeys)};
+    uint32_t* vbuf[2] = {reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys),
+                         reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + SM::kVals)};
+    __shared__ TileShared<LB> sh;
+    uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + 2 * SM::kVals);
 
     const int tid = threadIdx.x;
     const int shift = 8 * plan->digit[slot];
@@ -616,14 +703,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     nd.on = slot + 1 < na;
     nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
     nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
-    nd.hist_a = smem_addr(s_nhist);
+    nd.hist_a = smem_addr(sh.nhist);
     // TMA needs 16-byte aligned global sources (tiles are 16-byte multiples)
     const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
                      (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
-    const uint32_t mbar_a[2] = {smem_addr(&s_mbar[0]), smem_addr(&s_mbar[1])};
+    const uint32_t mbar_a[2] = {smem_addr(&sh.mbar[0]), smem_addr(&sh.mbar[1])};
     const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
 
-    auto prefetch = [&](uint32_t t, int b) {  // thread 0 only
+    auto prefetch = [&](uint32_t t, int b) {  // one thread only
         if (tma && t < ntiles && n - (uint64_t)t * TILE >= (uint64_t)TILE) {
             fence_proxy_async();
             mbar_expect_tx(mbar_a[b], tx_bytes);
@@ -643,38 +730,43 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
             const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (lane == 31) s_wsum64[tid >> 5] = incl;
-        s_goff[tid] = incl - c;
-        s_nhist[tid] = 0;
+        if (lane == 31) sh.wsum64[tid >> 5] = incl;
+        sh.goff[tid] = (typename TileShared<LB>::OFF)(incl - c);
+        sh.nhist[tid] = 0;
     }
-    for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_whist[i] = 0;
+    for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
+    if constexpr (MATCH_SMEM)
+        for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_match[i] = 0;
     if (tid == THREADS - 1) {
         mbar_init(mbar_a[0], 1);
         mbar_init(mbar_a[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-        s_tile[0] = t;
+        sh.tile[0] = t;
         prefetch(t, 0);
     }
     __syncthreads();
     if (tid < kRadix) {
         unsigned long long base = 0;
 #pragma unroll
-        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? s_wsum64[w] : 0ull;
-        s_goff[tid] += base;
+        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? sh.wsum64[w] : 0ull;
+        sh.goff[tid] += (typename TileShared<LB>::OFF)base;
     }
 
     int cur = 0;
     uint32_t parity = 0;  // bit b: phase parity of buffer b's mbarrier
     unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long prof_t = clock64();
+    (void)prof_t;
     for (;;) {
-        const uint32_t tile = s_tile[cur];
+        const uint32_t tile = sh.tile[cur];
         if (tile >= ntiles) break;
-        auto claim = [&]() {  // by a thread that sits out the look-back
+        // claim the next tile and stream it in during this tile's write-out
+        // (by a thread that sits out the look-back)
+        auto claim = [&]() {
             if (tid == THREADS - 1) {
                 const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-                s_tile[cur ^ 1] = t;
+                sh.tile[cur ^ 1] = t;
                 prefetch(t, cur ^ 1);
             }
         };
@@ -683,25 +775,21 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
         if (rem >= (uint64_t)TILE) {
             if (tma) {
-                B2S_PHASE(6);
                 mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
                 parity ^= 1u << cur;
                 B2S_PHASE(0);
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, MATCH>(
-                    claim,
-                    tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
-                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum, s_lbw, prof_acc, prof_t);
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true>(
+                    claim, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
+                    s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, MATCH>(
-                    claim,
-                    tile, TILE, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor, nd,
-                    s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum, s_lbw, prof_acc, prof_t);
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false>(
+                    claim, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
+                    s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, MATCH>(
-                claim,
-                tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, s_goff, lb_cur, shift, dxor,
-                nd, s_whist, kbuf[cur], vbuf[cur], s_gbase, s_wsum, s_lbw, prof_acc, prof_t);
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false>(
+                claim, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
+                nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
         }
         __syncthreads();
         B2S_PHASE(5);
@@ -712,8 +800,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         for (int k = 0; k < 8; ++k) atomicAdd(&b2s_phase_cycles[tid == 0 ? 0 : 1][k], prof_acc[k]);
 #endif
     // hand the next slot's digit counts to global memory once per CTA
-    if (nd.on && tid < kRadix && s_nhist[tid])
-        atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)s_nhist[tid]);
+    if (nd.on && tid < kRadix && sh.nhist[tid])
+        atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
 }
 
 template <typename U>
@@ -746,18 +834,19 @@ int onesweep_cfg() {
     return cfg;
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int MATCH = 0>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
 b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
                              void* lb) {
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
-    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, MATCH>;
+    constexpr size_t SMEM = SM::bytes;
+    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB>;
     static int occ = -1;  // per instantiation, per process (single device type)
     if (occ < 0) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SM::bytes));
+                                      (int)SMEM));
         int o = 0;
-        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SM::bytes));
+        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
         occ = o > 0 ? o : 1;
     }
     const uint64_t ntiles64 = (n + TILE - 1) / TILE;
@@ -767,7 +856,7 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
     const int slots = (int)sizeof(U);
     for (int s = 0; s < slots; ++s) {
         ctx->ev_pass[s] = record(ctx);
-        kern<<<grid, THREADS, SM::bytes, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
+        kern<<<grid, THREADS, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
                                                       region[(s + 1) & 1]);
         B2S_LAUNCHED();
     }
@@ -776,7 +865,7 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
 }
 
 // smallest tile over all configurations: sizes the look-back scratch
-constexpr int kMinTile = 512 * 6;
+constexpr int kMinTile = 512 * 6;  // smallest tile of any configuration
 
 template <typename U, bool VALS, typename LB>
 b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
@@ -786,12 +875,12 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
-        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 384, 16, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 4) return launch_passes_cfg<U, VALS, LB, 512, 16, 2, 1>(ctx, plan, ctr, n, lb);
-        if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 16, 2, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 6) return launch_passes_cfg<U, VALS, LB, 256, 16, 4, 1>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
+        if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 18, 2>(ctx, plan, ctr, n, lb);
+        // default: 10240-key tiles (measured best on B200: larger tiles amortise
+        // the per-tile 256-digit work; 22+ items spill)
+        return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 3>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);

@@ -12,8 +12,8 @@ import torch  # noqa: E402
 from paper_1105_6040_b200 import _lib  # noqa: E402
 from paper_1105_6040_b200.device import Context  # noqa: E402
 
-NAMES = ["tma_wait", "load+early_counts+sync", "digit_scan+sync", "rank", "lookback+sync",
-         "writeout+sync", "loop_top", "-"]
+NAMES = ["tma_wait+loop_top", "load+early_counts+sync", "digit_scan+sync", "rank",
+         "lookback+sync", "writeout+sync", "-", "-"]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 28
 ctx = Context(0)
 keys = ctx.gen_keys(n, 1, torch.uint32, shift=32)
@@ -26,7 +26,10 @@ ctx.sort(keys, out=out)
 torch.cuda.synchronize()
 _lib.lib().b2s_debug_phase_cycles(buf, 1)
 tiles = (n + 8191) // 8192
-print(f"look-back steps per tile (digit 0): {buf[7] / (tiles * 4):.2f}")
+print(f"look-back loop iterations per tile (warp 0): {buf[7] / (tiles * 4):.2f}; "
+      f"sync-step predecessors consumed {buf[6] % 1000000 / (tiles * 4):.2f}, "
+      f"unpublished hits {buf[6] // 1000000 / (tiles * 4):.2f}")
+buf[7] = buf[6] = 0
 for who, off in (("thread 0 (look-back warp)", 0), ("last thread", 8)):
     tot = sum(buf[off + k] for k in range(8)) or 1
-    print(who + ": " + ", ".join(f"{NAMES[k]} {100 * buf[off + k] / tot:.1f}%" for k in range(7)))
+    print(who + ": " + ", ".join(f"{NAMES[k]} {100 * buf[off + k] / tot:.1f}%" for k in range(6)))
