@@ -398,7 +398,6 @@ struct NextDigit {
 template <typename LB>
 struct TileShared {
     using OFF = LB;  // 32-bit offsets exactly when the look-back words are 32-bit (n < 2^30)
-    OFF gbase[kRadix];   // this tile's global base per digit (minus its tile start)
     OFF goff[kRadix];    // the slot's global digit offsets
     uint32_t nhist[kRadix];
     uint32_t start[kRadix];
@@ -413,9 +412,39 @@ struct TileShared {
 // One tile: keys come from `kbuf` (landed by TMA) when FROM_SMEM, else from
 // global memory; the tile is ranked, staged digit-sorted back into
 // `kbuf`/`vbuf`, and written out.
+// Write-out of a staged tile: runs of equal digits go to consecutive global
+// slots (consecutive threads, consecutive positions); the next slot's digit is
+// counted on the way out.
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS>
+__device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbuf,
+                                              const typename TileShared<LB>::OFF* gbase,
+                                              uint32_t tile_valid, U* __restrict__ dst,
+                                              uint32_t* __restrict__ vdst, int shift, uint32_t dxor,
+                                              const NextDigit nd) {
+    using OFF = typename TileShared<LB>::OFF;
+    const bool full = tile_valid == (uint32_t)(THREADS * ITEMS);
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = j * THREADS + threadIdx.x;
+        if (full || i < tile_valid) {
+            const U k = kbuf[i];
+            const OFF g = gbase[digit_of(k, shift, dxor)] + (OFF)i;
+#ifdef B2S_ABLATE_WRITE
+            if (k == (U)0x12345678 && g == 0)
+#endif
+            __stcs(dst + g, k);
+            if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
+#ifndef B2S_ABLATE_NEXTHIST
+            if (nd.on) red_add_shared(nd.hist_a + 4 * digit_of(k, nd.shift, nd.dxor), 1u);
+#endif
+        }
+    }
+}
+
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
-          typename Claim>
-__device__ __forceinline__ void onesweep_tile(const Claim& claim_next, uint32_t tile,
+          bool PIPE = false, typename Claim, typename Between>
+__device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Between& between,
+                                              typename TileShared<LB>::OFF* gbase_out, uint32_t tile,
                                               uint32_t tile_valid, uint64_t tile_base,
                                               const U* __restrict__ src, U* __restrict__ dst,
                                               const uint32_t* __restrict__ vsrc,
@@ -579,6 +608,13 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, uint32_t 
         }
     }
     B2S_PHASE(3);
+    if constexpr (PIPE) {
+        // this warp is done with its counters: clear them for the next tile,
+        // then write out the previous tile while the look-back reads land
+#pragma unroll
+        for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
+        between();
+    }
 
     // ---- decoupled look-back: one lane per digit. The first PRE predecessors
     // were fetched before ranking; later steps read LOOKBACK at a time
@@ -640,32 +676,18 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, uint32_t 
                 }
             }
         }
-        sh.gbase[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
+        gbase_out[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
     }
+    if constexpr (PIPE) return;  // the caller syncs; this tile is written next round
     __syncthreads();
     B2S_PHASE(4);
     claim_next();
 
-    // ---- write runs of equal digits: consecutive threads, consecutive slots;
-    // count the next slot's digit on the way out; clear this warp's counters
+    // ---- write runs of equal digits; clear this warp's counters
 #pragma unroll
     for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t i = j * THREADS + tid;
-        if (FULL || i < tile_valid) {
-            const U k = kbuf[i];
-            const OFF g = sh.gbase[digit_of(k, shift, dxor)] + (OFF)i;
-#ifdef B2S_ABLATE_WRITE
-            if (k == (U)0x12345678 && g == 0)
-#endif
-            __stcs(dst + g, k);
-            if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
-#ifndef B2S_ABLATE_NEXTHIST
-            if (nd.on) red_add_shared(nd.hist_a + 4 * digit_of(k, nd.shift, nd.dxor), 1u);
-#endif
-        }
-    }
+    writeout_tile<U, VALS, LB, THREADS, ITEMS>(kbuf, vbuf, gbase_out, tile_valid, dst, vdst, shift,
+                                               dxor, nd);
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
@@ -690,6 +712,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     uint32_t* vbuf[2] = {reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys),
                          reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + SM::kVals)};
     __shared__ TileShared<LB> sh;
+    __shared__ typename TileShared<LB>::OFF s_gbase[kRadix];
     uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + 2 * SM::kVals);
 
     const int tid = threadIdx.x;
@@ -763,6 +786,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         if (tile >= ntiles) break;
         // claim the next tile and stream it in during this tile's write-out
         // (by a thread that sits out the look-back)
+        auto noop = []() {};
         auto claim = [&]() {
             if (tid == THREADS - 1) {
                 const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
@@ -779,16 +803,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 parity ^= 1u << cur;
                 B2S_PHASE(0);
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true>(
-                    claim, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
+                    claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false>(
-                    claim, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
+                    claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
             }
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false>(
-                claim, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
+                claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
                 nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
         }
         __syncthreads();
@@ -800,6 +824,175 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         for (int k = 0; k < 8; ++k) atomicAdd(&b2s_phase_cycles[tid == 0 ? 0 : 1][k], prof_acc[k]);
 #endif
     // hand the next slot's digit counts to global memory once per CTA
+    if (nd.on && tid < kRadix && sh.nhist[tid])
+        atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
+}
+
+// Software-pipelined variant: tile k is ranked while tile k-1 (ranked in
+// the previous round) is written out, and tile k's look-back runs after that
+// write-out -- by then its prefetched predecessor window has landed and most
+// predecessors have posted inclusive prefixes, so the look-back rarely waits.
+// Three tile buffers rotate: k+1 landing by TMA, k being ranked in place,
+// k-1 being written out.
+template <typename U, bool VALS, int THREADS, int ITEMS>
+struct PipeSmem {
+    static constexpr int WARPS = THREADS / 32;
+    static constexpr int TILE = THREADS * ITEMS;
+    static constexpr size_t kCnt = (size_t)WARPS * (kRadix / 2) * 4;
+    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);
+    static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
+    static constexpr size_t kMatch = MATCH_SMEM ? (size_t)WARPS * kRadix * 4 : 0;
+    static constexpr size_t bytes = kCnt + 3 * kKeys + 3 * kVals + kMatch;
+};
+
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan* __restrict__ plan,
+                                                                      RadixCounters* __restrict__ ctr,
+                                                                      int slot, uint64_t n,
+                                                                      uint32_t ntiles,
+                                                                      LB* __restrict__ lb_cur,
+                                                                      LB* __restrict__ lb_next) {
+    using SM = PipeSmem<U, VALS, THREADS, ITEMS>;
+    constexpr int TILE = SM::TILE;
+    static_assert(THREADS >= kRadix, "one thread per digit is required");
+    static_assert(TILE < 65536, "packed 16-bit warp counters");
+
+    const int na = plan->num_active;
+    if (slot >= na) return;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);
+    U* kbuf[3];
+    uint32_t* vbuf[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+        kbuf[b] = reinterpret_cast<U*>(smem + SM::kCnt + b * SM::kKeys);
+        vbuf[b] = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 3 * SM::kKeys + b * SM::kVals);
+    }
+    uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 3 * SM::kKeys + 3 * SM::kVals);
+    __shared__ TileShared<LB> sh;
+    __shared__ typename TileShared<LB>::OFF s_gbase2[2][kRadix];
+    __shared__ alignas(8) unsigned long long s_mbar3[3];
+    __shared__ uint32_t s_tile3[3];
+
+    const int tid = threadIdx.x;
+    const int shift = 8 * plan->digit[slot];
+    const uint32_t dxor = plan->dxor[slot];
+    const U* src = static_cast<const U*>(plan->ksrc[slot]);
+    U* dst = static_cast<U*>(plan->kdst[slot]);
+    const uint32_t* vsrc = plan->vsrc[slot];
+    uint32_t* vdst = plan->vdst[slot];
+    NextDigit nd;
+    nd.on = slot + 1 < na;
+    nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
+    nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
+    nd.hist_a = smem_addr(sh.nhist);
+    const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                     (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
+    const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
+
+    auto prefetch = [&](uint32_t t, int b) {  // one thread only
+        if (tma && t < ntiles && n - (uint64_t)t * TILE >= (uint64_t)TILE) {
+            const uint32_t mb = smem_addr(&s_mbar3[b]);
+            fence_proxy_async();
+            mbar_expect_tx(mb, tx_bytes);
+            bulk_g2s(smem_addr(kbuf[b]), src + (uint64_t)t * TILE, (uint32_t)SM::kKeys, mb);
+            if constexpr (VALS)
+                bulk_g2s(smem_addr(vbuf[b]), vsrc + (uint64_t)t * TILE, (uint32_t)SM::kVals, mb);
+        }
+    };
+
+    if (tid < kRadix) {
+        const unsigned long long c = plan->hist[slot][tid];
+        unsigned long long incl = c;
+        const int lane = tid & 31;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) sh.wsum64[tid >> 5] = incl;
+        sh.goff[tid] = (typename TileShared<LB>::OFF)(incl - c);
+        sh.nhist[tid] = 0;
+    }
+    for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
+    if constexpr (MATCH_SMEM)
+        for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_match[i] = 0;
+    if (tid == THREADS - 1) {
+        for (int b = 0; b < 3; ++b) mbar_init(smem_addr(&s_mbar3[b]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
+        s_tile3[0] = t;
+        prefetch(t, 0);
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+        unsigned long long base = 0;
+#pragma unroll
+        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? sh.wsum64[w] : 0ull;
+        sh.goff[tid] += (typename TileShared<LB>::OFF)base;
+    }
+
+    int cur = 0;           // buffer of the current tile (ring of 3)
+    int prev = -1;         // buffer of the staged previous tile, -1 if none
+    uint32_t prev_valid = 0;
+    int gcur = 0;          // gbase slot of the current tile (ring of 2)
+    uint32_t parity = 0;   // bit b: phase parity of buffer b's mbarrier
+    unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_t = clock64();
+    (void)prof_t;
+    for (;;) {
+        const uint32_t tile = s_tile3[cur];
+        if (tile >= ntiles) break;
+        const int nxt = cur == 2 ? 0 : cur + 1;
+        if (tid == THREADS - 1) {  // claim tile k+1 into the buffer tile k-2 freed
+            const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
+            s_tile3[nxt] = t;
+            prefetch(t, nxt);
+        }
+        const uint64_t tile_base = (uint64_t)tile * TILE;
+        const uint64_t rem = n - tile_base;
+        if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
+        const int pb = prev;
+        const uint32_t pv = prev_valid;
+        const int pg = gcur ^ 1;
+        auto write_prev = [&]() {
+            if (pb >= 0)
+                writeout_tile<U, VALS, LB, THREADS, ITEMS>(kbuf[pb], vbuf[pb], s_gbase2[pg], pv, dst,
+                                                           vdst, shift, dxor, nd);
+        };
+        auto noop = []() {};
+        if (rem >= (uint64_t)TILE) {
+            if (tma) {
+                mbar_wait(smem_addr(&s_mbar3[cur]), (parity >> cur) & 1u);
+                parity ^= 1u << cur;
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true>(
+                    noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
+                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc,
+                    prof_t);
+            } else {
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true>(
+                    noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
+                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc,
+                    prof_t);
+            }
+            prev_valid = TILE;
+        } else {
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true>(
+                noop, write_prev, s_gbase2[gcur], tile, (uint32_t)rem, tile_base, src, dst, vsrc,
+                vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc,
+                prof_t);
+            prev_valid = (uint32_t)rem;
+        }
+        __syncthreads();
+        prev = cur;
+        gcur ^= 1;
+        cur = nxt;
+    }
+    if (prev >= 0)
+        writeout_tile<U, VALS, LB, THREADS, ITEMS>(kbuf[prev], vbuf[prev], s_gbase2[gcur ^ 1],
+                                                   prev_valid, dst, vdst, shift, dxor, nd);
+    __syncthreads();
     if (nd.on && tid < kRadix && sh.nhist[tid])
         atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
 }
@@ -864,6 +1057,34 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
     return B2S_OK;
 }
 
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+b2s_status launch_pipe_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
+    using SM = PipeSmem<U, VALS, THREADS, ITEMS>;
+    constexpr int TILE = SM::TILE;
+    constexpr size_t SMEM = SM::bytes;
+    auto kern = onesweep_pipe_kernel<U, VALS, LB, THREADS, ITEMS, MINB>;
+    static int occ = -1;
+    if (occ < 0) {
+        B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+        int o = 0;
+        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
+        occ = o > 0 ? o : 1;
+    }
+    const uint64_t ntiles64 = (n + TILE - 1) / TILE;
+    const uint32_t ntiles = (uint32_t)ntiles64;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ * ctx->num_sms);
+    LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
+    const int slots = (int)sizeof(U);
+    for (int s = 0; s < slots; ++s) {
+        ctx->ev_pass[s] = record(ctx);
+        kern<<<grid, THREADS, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
+                                                   region[(s + 1) & 1]);
+        B2S_LAUNCHED();
+    }
+    ctx->ev_pass[slots] = record(ctx);
+    return B2S_OK;
+}
+
 // smallest tile over all configurations: sizes the look-back scratch
 constexpr int kMinTile = 512 * 6;  // smallest tile of any configuration
 
@@ -878,6 +1099,9 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
         if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 18, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 6) return launch_pipe_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 7) return launch_pipe_cfg<U, VALS, LB, 512, 14, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 8) return launch_pipe_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
         // default: 10240-key tiles (measured best on B200: larger tiles amortise
         // the per-tile 256-digit work; 22+ items spill)
         return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
