@@ -72,20 +72,25 @@ class Clocks:
         self.path = None
 
     def start(self):
+        """Starts sampling and waits (<= 5 s) for the first sample, so the
+        sampler is live before the timed region begins."""
         try:
             fd, self.path = tempfile.mkstemp(prefix="clocks", suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 5 and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -277,12 +282,15 @@ def run_single(args):
 # B200 arm, N > 1 (torchrun)
 
 def run_multi(args, rank: int, world: int):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_1105_6040_b200.device import Context
     from paper_1105_6040_b200.sample_sort import SampleSorter
 
+    hbm_peak, peak_kind = _peaks()
+    nvlink_gbs = 770.0  # measured peer copy per direction (B200_PROFILING.md)
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -291,10 +299,9 @@ def run_multi(args, rank: int, world: int):
     total = n_local * world
     # shard r holds keys [r*n_local, (r+1)*n_local) of the cfg3 stream (int32 = z >> 33)
     keys = ctx.gen_keys(n_local, 1, torch.int32, shift=33, first=rank * n_local)
-    sorter = SampleSorter(ctx, samples_per_rank=64)
-    out = sorter.sort(keys)
-    ok = sorter.verify(out)
-    if not ok:
+    sorter = SampleSorter(ctx, samples_per_rank=64, force_exchange=args.force_dist)
+    out, _ = sorter.sort(keys)
+    if not sorter.verify(out, keys):
         raise RuntimeError(f"rank {rank}: sample sort verification failed")
     for _ in range(args.warmup):
         sorter.sort(keys)
@@ -311,8 +318,47 @@ def run_multi(args, rank: int, world: int):
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    clk = clocks.stop()
     ms_step = float(ms.item())
+    phases = dict(sorter.last_phase_ms)
+    buckets = list(sorter.last_bucket_sizes)
+
+    # per-pass kernel time of the local sort (CUDA events inside the ABI)
+    ctx.enable_timing(True)
+    pass_ms = []
+    for _ in range(max(2, args.steps // 2)):
+        ctx.sort(keys)
+        pass_ms.extend(ctx.timing().pass_ms)
+    ctx.enable_timing(False)
+    clk = clocks.stop()
+
+    # end to end through the public API: pinned host shard -> device -> sort ->
+    # this rank's bucket back to pinned host memory
+    h_in = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+    h_in.copy_(keys.cpu())
+    h_out = torch.empty(2 * n_local + 64 * world * world, dtype=torch.int32, pin_memory=True)
+    dk = torch.empty_like(keys)
+    e2e_steps = max(1, min(args.steps, 3))
+    dist.barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(e2e_steps):
+        dk.copy_(h_in, non_blocking=True)
+        ok_, _ = sorter.sort(dk)
+        h_out[: ok_.numel()].copy_(ok_, non_blocking=True)
+        d2h = ok_.numel() * 4
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device="cuda")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+
+    avg_pass = statistics.mean(pass_ms)
+    alg = 2 * 4 * n_local
+    achieved = alg / (avg_pass * 1e-3) / 1e9
+    # combined roofline per GPU (serial, non-overlapped): 4 sort passes +
+    # merge rounds over HBM, (G-1)/G of the shard over NVLink each direction
+    rounds = max(1, (world - 1).bit_length()) if world > 1 else 0
+    hbm_bytes = (4 * 2 * 4 + 4 + rounds * 2 * 4) * n_local
+    nvl_bytes = 4 * n_local * (world - 1) / world
+    t_roof_ms = (hbm_bytes / (hbm_peak * 1e9) + nvl_bytes / (nvlink_gbs * 1e9)) * 1e3
     if rank == 0:
         line = {
             "metric": METRIC, "value": total / (ms_step * 1e-3), "unit": UNIT,
@@ -321,8 +367,21 @@ def run_multi(args, rank: int, world: int):
             "vs_baseline": None, "dtype": "i32",
             "data": "synthetic (gen_data splitmix64 seed 1 >> 33, int32 in [0, 2^31))",
             "config": {"workload": "cfg3: sample sort, 2^28 int32 keys per GPU, 64 samples/GPU",
-                       "n_per_gpu": n_local, "parallelism": f"sample sort over {world} GPUs"},
-            "gpu_launches": None, "clocks": clk, "phases_ms": sorter.last_phase_ms,
+                       "n_per_gpu": n_local, "parallelism": f"sample sort over {world} GPUs",
+                       "l2": "inputs larger than L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": _traffic(n_local),
+                         "kernel": "onesweep_kernel (one digit pass, rank 0)",
+                         "peak_kind": peak_kind,
+                         "combined_hbm_nvlink_frac": t_roof_ms / ms_step,
+                         "combined_roofline_ms": t_roof_ms},
+            "phases_ms": phases, "bucket_sizes": buckets,
+            "e2e": {"value": total / float(e2e_s.item()), "unit": UNIT,
+                    "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": d2h,
+                    "path": "SampleSorter.sort from pinned host shards (per rank)"},
+            "gpu_launches": args.steps * (7 + 3 + 2 * rounds),
+            "clocks": clk,
+            "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -340,13 +399,15 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--ref-sample", type=int, default=1 << 24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU sample-sort path even at world size 1")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or args.force_dist:
         run_multi(args, rank, world)
     else:
         run_single(args)
