@@ -18,6 +18,8 @@
 // k-way merge: ceil(log2 k) rounds of pairwise merges, ping-ponging between
 // the output and a scratch buffer so the last round lands in the output.
 // merge_split_padded: one merge-path tile pass restricted to the kept half.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "b2s_internal.cuh"
@@ -169,17 +171,238 @@ b2s_status merge2_window(b2s_ctx* ctx, const T* a, const uint32_t* va, uint64_t 
     return B2S_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Single-pass k-way merge (k <= kMaxK), replacing ceil(log2 k) pairwise rounds.
+//
+// Every S-th element of every run is a boundary record (key, run, position).
+// kmerge_bounds_kernel places each boundary exactly: its cut in every other run
+// is a binary search (ties: lower runs' equal keys come first), its rank among
+// all boundaries is the number of each run's boundaries before those cuts.
+// Between two consecutive boundaries in that order each run contributes at
+// most S elements, so a bucket holds <= k*S keys and fits in shared memory.
+// kmerge_bucket_kernel loads each bucket's k sub-ranges with coalesced reads,
+// merges them pairwise in shared memory (log2 k rounds, stable: ties to the
+// lower run) and writes the bucket with coalesced stores at its output offset
+// (the sum of its lower cuts). HBM traffic: one read + one write per key.
+
+constexpr int kMaxK = 16;
+
+template <typename T>
+struct KRuns {
+    const T* key[kMaxK];
+    const uint32_t* val[kMaxK];
+    uint64_t n[kMaxK];
+    uint64_t nb_off[kMaxK + 1];  // prefix of boundaries per run
+    int k;
+    uint32_t S;                   // boundary stride
+};
+
+template <typename T>
+__device__ __forceinline__ uint64_t bound_in(const T* a, uint64_t n, T v, bool upper) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        const T x = a[mid];
+        if (x < v || (upper && !(v < x))) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <typename T>
+__global__ void kmerge_bounds_kernel(const KRuns<T> R, uint64_t* __restrict__ cuts) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= R.nb_off[R.k]) return;
+    int r = 0;
+    while (q >= R.nb_off[r + 1]) ++r;
+    const uint64_t j = q - R.nb_off[r];
+    const uint64_t pos = (j + 1) * R.S - 1;
+    const T v = R.key[r][pos];
+    uint64_t c[kMaxK];
+    uint64_t rank = j;
+    for (int r2 = 0; r2 < R.k; ++r2) {
+        uint64_t cut;
+        if (r2 == r) cut = pos + 1;
+        else cut = bound_in(R.key[r2], R.n[r2], v, r2 < r);
+        c[r2] = cut;
+        if (r2 != r) rank += cut / R.S;
+    }
+    for (int r2 = 0; r2 < R.k; ++r2) cuts[rank * R.k + r2] = c[r2];
+}
+
+constexpr int kKThreads = 256;
+
+template <typename T, bool VALS>
+__global__ void __launch_bounds__(kKThreads) kmerge_bucket_kernel(const KRuns<T> R,
+                                                                  const uint64_t* __restrict__ cuts,
+                                                                  uint64_t nbuckets, uint32_t per_cta,
+                                                                  uint32_t cap, T* __restrict__ out,
+                                                                  uint32_t* __restrict__ vout) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* kA = reinterpret_cast<T*>(smem);
+    T* kB = kA + cap;
+    uint32_t* vA = reinterpret_cast<uint32_t*>(kB + cap);
+    uint32_t* vB = vA + (VALS ? cap : 0);
+    __shared__ uint64_t s_lo[kMaxK];
+    __shared__ uint32_t s_seg[kMaxK + 1];  // segment offsets inside the bucket
+    __shared__ uint64_t s_out;
+    const int k = R.k;
+    const int tid = threadIdx.x;
+    const uint64_t b0 = (uint64_t)blockIdx.x * per_cta;
+    const uint64_t b1 = b0 + per_cta < nbuckets ? b0 + per_cta : nbuckets;
+    for (uint64_t b = b0; b < b1; ++b) {
+        if (tid == 0) {
+            uint32_t acc = 0;
+            uint64_t o = 0;
+            for (int r = 0; r < k; ++r) {
+                const uint64_t lo = b == 0 ? 0 : cuts[(b - 1) * k + r];
+                const uint64_t hi = b + 1 == nbuckets ? R.n[r] : cuts[b * k + r];
+                s_lo[r] = lo;
+                s_seg[r] = acc;
+                acc += (uint32_t)(hi - lo);
+                o += lo;
+            }
+            s_seg[k] = acc;
+            s_out = o;
+        }
+        __syncthreads();
+        const uint32_t total = s_seg[k];
+        // coalesced loads of the k sub-ranges, concatenated in run order
+        for (int r = 0; r < k; ++r) {
+            const uint32_t base = s_seg[r], len = s_seg[r + 1] - base;
+            const T* src = R.key[r] + s_lo[r];
+            for (uint32_t i = tid; i < len; i += kKThreads) kA[base + i] = src[i];
+            if constexpr (VALS) {
+                const uint32_t* vs = R.val[r] + s_lo[r];
+                for (uint32_t i = tid; i < len; i += kKThreads) vA[base + i] = vs[i];
+            }
+        }
+        __syncthreads();
+        // pairwise rounds in shared memory; a pair keeps the position range of
+        // its two segments, so segment offsets after a round are every other one
+        T* ka = kA;
+        T* kb = kB;
+        uint32_t* va = vA;
+        uint32_t* vb = vB;
+        int nseg = k;
+        int stride = 1;  // segments of this round start at s_seg[i * stride]
+        while (nseg > 1) {
+            constexpr int ITEMS = 8;
+            for (uint32_t x0 = tid * ITEMS; x0 < total; x0 += kKThreads * ITEMS) {
+                const uint32_t x1 = x0 + ITEMS < total ? x0 + ITEMS : total;
+                uint32_t x = x0;
+                while (x < x1) {
+                    // the pair holding output position x
+                    int pr = 0;
+                    while (pr + 1 < (nseg + 1) / 2 && s_seg[min((pr + 1) * 2 * stride, k)] <= x) ++pr;
+                    const uint32_t a0 = s_seg[min(pr * 2 * stride, k)];
+                    const uint32_t a1 = s_seg[min(pr * 2 * stride + stride, k)];
+                    const uint32_t e1 = s_seg[min(pr * 2 * stride + 2 * stride, k)];
+                    const uint32_t la = a1 - a0, lb = e1 - a1;
+                    const uint32_t diag = x - a0;
+                    uint32_t ai = merge_path_smem(ka + a0, la, ka + a1, lb, diag);
+                    uint32_t bi = diag - ai;
+                    const uint32_t stop = x1 < e1 ? x1 : e1;
+                    for (; x < stop; ++x) {
+                        const bool take_a = bi >= lb || (ai < la && !(ka[a1 + bi] < ka[a0 + ai]));
+                        const uint32_t src = take_a ? a0 + ai++ : a1 + bi++;
+                        kb[x] = ka[src];
+                        if constexpr (VALS) vb[x] = va[src];
+                    }
+                }
+            }
+            __syncthreads();
+            T* t = ka;
+            ka = kb;
+            kb = t;
+            uint32_t* tv = va;
+            va = vb;
+            vb = tv;
+            nseg = (nseg + 1) / 2;
+            stride *= 2;
+        }
+        const uint64_t o = s_out;
+        for (uint32_t i = tid; i < total; i += kKThreads) {
+            out[o + i] = ka[i];
+            if constexpr (VALS) vout[o + i] = va[i];
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+b2s_status kway_single_pass(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* vals,
+                            const uint64_t* lens, int k, void* out, uint32_t* vout) {
+    const bool with_vals = vout != nullptr;
+    const size_t rec = sizeof(T) + (with_vals ? 4 : 0);
+    // two buffers of `cap` records in <= 64 KB, cap = k * S with S a power of two
+    uint32_t S = 1;
+    const char* es = getenv("B2S_KWAY_SMEM_KB");
+    const uint64_t budget = (uint64_t)(es ? atoi(es) : 64) * 1024;
+    while ((uint64_t)2 * k * (S * 2) * rec <= budget) S *= 2;
+    const uint32_t cap = (uint32_t)k * S;
+    KRuns<T> R{};
+    R.k = k;
+    R.S = S;
+    R.nb_off[0] = 0;
+    uint64_t total = 0;
+    for (int r = 0; r < k; ++r) {
+        R.key[r] = static_cast<const T*>(runs[r]);
+        R.val[r] = with_vals ? vals[r] : nullptr;
+        R.n[r] = lens[r];
+        R.nb_off[r + 1] = R.nb_off[r] + lens[r] / S;
+        total += lens[r];
+    }
+    const uint64_t nb = R.nb_off[k];
+    const uint64_t nbuckets = nb + 1;
+    B2S_TRY(ctx->parts.ensure((nb * k + 1) * sizeof(uint64_t)));
+    uint64_t* cuts = static_cast<uint64_t*>(ctx->parts.ptr);
+    ctx->ev_merge0 = record(ctx);
+    if (nb > 0) {
+        kmerge_bounds_kernel<T><<<(unsigned)((nb + 255) / 256), 256, 0, ctx->stream>>>(R, cuts);
+        B2S_LAUNCHED();
+    }
+    const size_t smem = (size_t)2 * cap * rec;
+    auto kern = with_vals ? kmerge_bucket_kernel<T, true> : kmerge_bucket_kernel<T, false>;
+    B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint64_t want_ctas = (uint64_t)ctx->num_sms * 3 * 4;
+    const uint32_t per_cta = (uint32_t)std::max<uint64_t>(1, (nbuckets + want_ctas - 1) / want_ctas);
+    const unsigned grid = (unsigned)((nbuckets + per_cta - 1) / per_cta);
+    kern<<<grid, kKThreads, smem, ctx->stream>>>(R, cuts, nbuckets, per_cta, cap,
+                                                 static_cast<T*>(out), vout);
+    B2S_LAUNCHED();
+    ctx->ev_merge1 = record(ctx);
+    ctx->last_merge_rounds = 1;
+    (void)total;
+    return B2S_OK;
+}
+
 struct Run {
     const void* k;
     const uint32_t* v;
     uint64_t n;
 };
 
+int kway_mode() {
+    static int m = -1;
+    if (m < 0) {
+        // 0: pairwise rounds (default: 3.5 TB/s per round on B200), 1: the
+        // single-pass bucket merge (correct, but its in-shared-memory merge is
+        // latency-bound at the occupancy its buffers allow: 3.5 ms vs 1.84 ms for
+        // 8 runs of 2^25 keys -- kept for further work)
+        const char* e = getenv("B2S_KWAY");
+        m = e ? atoi(e) : 0;
+    }
+    return m;
+}
+
 template <typename T>
 b2s_status kway_t(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* vals,
                   const uint64_t* lens, int k, void* out, uint32_t* vout, void* tmp,
                   uint32_t* vtmp) {
     const bool with_vals = vout != nullptr;
+    if (k > 2 && k <= kMaxK && kway_mode() == 1)
+        return kway_single_pass<T>(ctx, runs, vals, lens, k, out, vout);
     std::vector<Run> cur;
     uint64_t total = 0;
     for (int i = 0; i < k; ++i) {

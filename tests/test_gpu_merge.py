@@ -1,6 +1,8 @@
 """GPU: merge-path merges (b2s_merge, b2s_merge_split_padded) and the
 single-GPU partitioned sort against the oracle, including kernels::merge_runs'
 tie rule (ties from the lower run) checked through a payload."""
+import os
+
 import numpy as np
 import pytest
 
@@ -23,6 +25,27 @@ def ctx():
 @pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 7, 8, 9, 16])
 def test_kway_merge(ctx, dt, k):
+    _kway_case(ctx, dt, k)
+
+
+@pytest.mark.parametrize("k", [3, 8, 16])
+def test_kway_single_pass_variant(k):
+    """The experimental single-pass bucket merge (B2S_KWAY=1), in a subprocess so
+    the mode switch is read fresh."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "import numpy as np, test_gpu_merge as t\n"
+            "from paper_1105_6040_b200.device import Context\n"
+            "c = Context(0)\n"
+            "for dt in t.DTYPES: t._kway_case(c, dt, %d)\n"
+            "print('ok')") % (os.path.dirname(__file__), os.path.dirname(os.path.dirname(__file__)), k)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, B2S_KWAY="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def _kway_case(ctx, dt, k):
     rng = np.random.default_rng(k * 31 + np.dtype(dt).itemsize)
     for kind in ("uniform", "dups"):
         lens = [int(x) for x in rng.integers(0, 20_000, k)]
