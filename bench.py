@@ -119,7 +119,11 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # reference CPU arm (oracle/_ref = the reference library compiled from source)
 
-def cpu_reference(sample_n: int, reps: int = 3):
+WORKLOAD_1 = "cfg2: 2^28 uint32 keys, p=1, 4 x 8-bit LSD passes"
+WORKLOAD_N = "cfg3: sample sort, 2^28 int32 keys per GPU, 64 samples/GPU"
+
+
+def cpu_reference(sample_n: int, reps: int = 3, shift: int = 32):
     """parallel::scatter_merge_sort (merge, wall mode, p = k = host threads) on
     `sample_n` keys of the workload's distribution widened to int64 (the
     reference's only Element type); run_benchmark's semantics: median of reps
@@ -129,7 +133,7 @@ def cpu_reference(sample_n: int, reps: int = 3):
     import oracle
     threads = max(1, min(os.cpu_count() or 1, 64))
     z = oracle.gen_data(sample_n, 1).view(np.uint64)
-    data = (z >> np.uint64(32)).astype(np.int64)
+    data = (z >> np.uint64(shift)).astype(np.int64)
     if oracle.ref_available():
         kind = "reference"
         times = []
@@ -146,7 +150,7 @@ def cpu_reference(sample_n: int, reps: int = 3):
     if not (out[1:] >= out[:-1]).all():
         raise RuntimeError("CPU baseline produced unsorted output")
     return {"value": sample_n / t, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{sample_n} keys (cfg2 distribution widened to int64), "
+            "sample": f"{sample_n} keys (gen_data >> {shift}, widened to int64), "
                       f"scatter_merge_sort merge p=k={threads}, median of {reps} wall-mode reps"}
 
 
@@ -154,10 +158,12 @@ def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
     sample_n = args.ref_sample
+    multi = max(args.gpus, world) > 1
+    shift = 33 if multi else 32  # cfg3 int32 in [0, 2^31) / cfg2 full-range uint32
     vals = []
     base = None
     for i in range(args.warmup + args.steps):
-        b = cpu_reference(sample_n, reps=1)
+        b = cpu_reference(sample_n, reps=1, shift=shift)
         if i >= args.warmup:
             vals.append(b["value"])
         base = b
@@ -168,8 +174,9 @@ def run_reference_arm(args, rank: int, world: int):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (gen_data splitmix64 seed 1)",
-        "config": {"workload": "cfg2 sample on host CPU", "n": sample_n,
-                   "p": base["cores"], "algorithm": "merge"},
+        "config": {"workload": WORKLOAD_N if multi else WORKLOAD_1, "sample_n": sample_n,
+                   "p": base["cores"], "algorithm": "merge",
+                   "note": "reference CPU path on a bounded sample of the workload"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
                          "sample": base["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -250,13 +257,13 @@ def run_single(args):
     alg_bytes = 2 * 4 * n  # read + write of every 4-byte key per pass
     achieved = alg_bytes / (avg_pass * 1e-3) / 1e9
     value = n / (ms_step * 1e-3)
-    cpu = cpu_reference(args.cpu_sample, reps=3) if not args.no_cpu else None
+    cpu = cpu_reference(args.cpu_sample, reps=3, shift=32) if not args.no_cpu else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (gen_data splitmix64 seed 1 >> 32, uniform 32-bit)",
-        "config": {"workload": "cfg2: 2^28 uint32 keys, p=1, 4 x 8-bit LSD passes",
+        "config": {"workload": WORKLOAD_1,
                    "n": n, "p": 1, "key_bytes": 4,
                    "l2": "inputs (1 GiB) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -366,7 +373,7 @@ def run_multi(args, rank: int, world: int):
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "i32",
             "data": "synthetic (gen_data splitmix64 seed 1 >> 33, int32 in [0, 2^31))",
-            "config": {"workload": "cfg3: sample sort, 2^28 int32 keys per GPU, 64 samples/GPU",
+            "config": {"workload": WORKLOAD_N,
                        "n_per_gpu": n_local, "parallelism": f"sample sort over {world} GPUs",
                        "l2": "inputs larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
