@@ -282,9 +282,13 @@ struct OnesweepSmem {
     static constexpr size_t kKeys = (size_t)TILE * sizeof(U);         // one tile buffer
     static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
     static constexpr size_t kMatch = MATCH_SMEM ? (size_t)WARPS * kRadix * 4 : 0;
-    // counters | keys[2] | vals[2] | match masks: tile i+1 streams in by TMA
-    // while tile i is ranked in place in its own buffer
-    static constexpr size_t bytes = kCnt + 2 * kKeys + 2 * kVals + kMatch;
+    // unpacked early counts; they share the match masks' space (both are all
+    // zero between uses: the digit section clears the counts, every ranking
+    // step clears its mask)
+    static constexpr size_t kEarly = MATCH_SMEM ? 0 : (size_t)WARPS * kRadix * 4;
+    // counters | keys[2] | vals[2] | match masks | early counts: tile i+1
+    // streams in by TMA while tile i is ranked in place in its own buffer
+    static constexpr size_t bytes = kCnt + 2 * kKeys + 2 * kVals + kMatch + kEarly;
 };
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier ----------
@@ -391,7 +395,7 @@ struct NextDigit {
     int shift;
     uint32_t dxor;
     bool on;
-    uint32_t hist_a;  // shared address of the next slot's digit counters
+    uint32_t* hist;  // the next slot's digit counters (shared memory)
 };
 
 // Shared state of one CTA besides the tile buffers.
@@ -435,7 +439,7 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
             __stcs(dst + g, k);
             if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
 #ifndef B2S_ABLATE_NEXTHIST
-            if (nd.on) red_add_shared(nd.hist_a + 4 * digit_of(k, nd.shift, nd.dxor), 1u);
+            if (nd.on) atomicAdd(nd.hist + digit_of(k, nd.shift, nd.dxor), 1u);  // ATOMS.POPC.INC
 #endif
         }
     }
@@ -451,7 +455,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                                               uint32_t* __restrict__ vdst, LB* __restrict__ lb_cur,
                                               int shift, uint32_t dxor, const NextDigit nd,
                                               uint32_t* s_cnt, U* kbuf, uint32_t* vbuf,
-                                              uint32_t* s_match, TileShared<LB>& sh,
+                                              uint32_t* s_match, uint32_t* s_early,
+                                              TileShared<LB>& sh,
                                               unsigned long long* prof_acc,
                                               long long& prof_t) {
     (void)prof_acc;
@@ -502,12 +507,15 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         }
     }
 
-    // ---- early counts: per-warp digit histogram (packed 16-bit halves)
+    // ---- early counts: per-warp digit histogram. Even and odd digits count
+    // into separate words with +1 increments (ATOMS.POPC.INC aggregates lanes
+    // that hit the same counter); the digit section packs them into 16-bit
+    // pairs for ranking.
+    uint32_t* ecnt = s_early + warp * kRadix;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t d = digit_of(keys[j], shift, dxor);
-        const uint32_t a = cnt_a + 4 * (d >> 1);
-        if (FULL || wbase + j * 32 + lane < tile_valid) red_add_shared(a, 1u << (16 * (d & 1)));
+        if (FULL || wbase + j * 32 + lane < tile_valid) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
     }
     __syncthreads();  // also: every warp has read its keys out of kbuf
     B2S_PHASE(1);
@@ -518,7 +526,10 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     if (tid < HALF) {
 #pragma unroll 4
         for (int w = 0; w < WARPS; ++w) {
-            const uint32_t c = s_cnt[w * HALF + tid];
+            uint32_t* e = s_early + w * kRadix;
+            const uint32_t c = e[tid] | (e[HALF + tid] << 16);
+            e[tid] = 0;
+            e[HALF + tid] = 0;
             s_cnt[w * HALF + tid] = pair;
             pair += c;
         }
@@ -714,6 +725,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     __shared__ TileShared<LB> sh;
     __shared__ typename TileShared<LB>::OFF s_gbase[kRadix];
     uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + 2 * SM::kVals);
+    uint32_t* s_early = MATCH_SMEM ? s_match : s_match + SM::kMatch / 4;
 
     const int tid = threadIdx.x;
     const int shift = 8 * plan->digit[slot];
@@ -726,7 +738,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     nd.on = slot + 1 < na;
     nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
     nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
-    nd.hist_a = smem_addr(sh.nhist);
+    nd.hist = sh.nhist;
     // TMA needs 16-byte aligned global sources (tiles are 16-byte multiples)
     const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
                      (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
@@ -758,6 +770,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         sh.nhist[tid] = 0;
     }
     for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
+    for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_early[i] = 0;
     if constexpr (MATCH_SMEM)
         for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_match[i] = 0;
     if (tid == THREADS - 1) {
@@ -804,16 +817,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 B2S_PHASE(0);
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
+                    s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
+                    s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
             }
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false>(
                 claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
-                nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc, prof_t);
+                nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
         }
         __syncthreads();
         B2S_PHASE(5);
@@ -842,7 +855,8 @@ struct PipeSmem {
     static constexpr size_t kKeys = (size_t)TILE * sizeof(U);
     static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
     static constexpr size_t kMatch = MATCH_SMEM ? (size_t)WARPS * kRadix * 4 : 0;
-    static constexpr size_t bytes = kCnt + 3 * kKeys + 3 * kVals + kMatch;
+    static constexpr size_t kEarly = MATCH_SMEM ? 0 : (size_t)WARPS * kRadix * 4;
+    static constexpr size_t bytes = kCnt + 3 * kKeys + 3 * kVals + kMatch + kEarly;
 };
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
@@ -870,6 +884,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
         vbuf[b] = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 3 * SM::kKeys + b * SM::kVals);
     }
     uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 3 * SM::kKeys + 3 * SM::kVals);
+    uint32_t* s_early = MATCH_SMEM ? s_match : s_match + SM::kMatch / 4;
     __shared__ TileShared<LB> sh;
     __shared__ typename TileShared<LB>::OFF s_gbase2[2][kRadix];
     __shared__ alignas(8) unsigned long long s_mbar3[3];
@@ -886,7 +901,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
     nd.on = slot + 1 < na;
     nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
     nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
-    nd.hist_a = smem_addr(sh.nhist);
+    nd.hist = sh.nhist;
     const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
                      (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
     const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
@@ -916,6 +931,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
         sh.nhist[tid] = 0;
     }
     for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
+    for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_early[i] = 0;
     if constexpr (MATCH_SMEM)
         for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_match[i] = 0;
     if (tid == THREADS - 1) {
@@ -968,19 +984,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
                 parity ^= 1u << cur;
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
-                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc,
+                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
-                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc,
+                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             }
             prev_valid = TILE;
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true>(
                 noop, write_prev, s_gbase2[gcur], tile, (uint32_t)rem, tile_base, src, dst, vsrc,
-                vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, sh, prof_acc,
+                vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                 prof_t);
             prev_valid = (uint32_t)rem;
         }
