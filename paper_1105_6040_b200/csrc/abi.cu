@@ -180,6 +180,11 @@ b2s_status b2s_create(int device, b2s_ctx** out) {
         b2s_destroy(ctx);
         return st;
     }
+    if (st == B2S_OK) st = probe_lane_order(ctx, &ctx->atomic_rank);
+    if (st != B2S_OK) {
+        b2s_destroy(ctx);
+        return st;
+    }
     timing_reset(ctx);
     *out = ctx;
     return B2S_OK;

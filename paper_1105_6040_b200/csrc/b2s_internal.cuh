@@ -119,6 +119,9 @@ struct b2s_ctx {
     int last_passes_possible = 0;
     int last_merge_rounds = 0;
     bool have_sort = false, have_merge = false;
+    // lane-ordered shared atomics verified on this device (onesweep ranks by
+    // atomics instead of ballot matching); see b2s::probe_lane_order
+    bool atomic_rank = false;
 };
 
 namespace b2s {
@@ -146,6 +149,7 @@ b2s_status select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count, 
                             b2s_sample* splitters);
 b2s_status bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n, int rank,
                          const b2s_sample* splitters, int nparts, uint64_t* bounds);
+b2s_status probe_lane_order(b2s_ctx* ctx, bool* ok);
 b2s_status gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
                     int shift, void* out);
 b2s_status check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,

@@ -35,6 +35,8 @@
 
 #include <stdlib.h>
 
+#include <string>
+
 #include "b2s_internal.cuh"
 
 #ifdef B2S_PHASE_PROFILE
@@ -446,7 +448,7 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
-          bool PIPE = false, typename Claim, typename Between>
+          bool PIPE, int RANK, typename Claim, typename Between>
 __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Between& between,
                                               typename TileShared<LB>::OFF* gbase_out, uint32_t tile,
                                               uint32_t tile_valid, uint64_t tile_base,
@@ -589,6 +591,18 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #ifdef B2S_ABLATE_RANK
         const uint32_t peers = 1u << lane;
 #else
+        uint32_t r;
+        if constexpr (RANK == 1) {
+            // lane-ordered shared atomics: lanes adding to the same counter in one
+            // warp instruction receive old values in ascending lane order on this
+            // device (verified at context creation by b2s::probe_lane_order), so
+            // the returned count is directly the stable rank -- no match needed
+            const uint32_t sh16 = 16 * (d & 1);
+            const uint32_t a = cnt_a + 4 * ((d >> 1) & (HALF - 1));
+            const uint32_t old = FULL ? atom_add_shared(a, 1u << sh16)
+                                      : atom_add_shared(valid ? a : dummy_a, valid ? 1u << sh16 : 0u);
+            r = (old >> sh16) & 0xFFFFu;
+        } else {
         uint32_t peers;
         if (MATCH_SMEM && (B2S_MATCH_HYBRID == 1 || (j % B2S_MATCH_HYBRID) != 0)) {
             // odd items: OR-mask match through shared memory (LSU pipe) to
@@ -608,7 +622,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         const uint32_t old = atom_add_shared(claim ? cnt_a + 4 * ((d >> 1) & (HALF - 1)) : dummy_a,
                                              claim ? (below + 1) << sh16 : 0u);
         const uint32_t base = (__shfl_sync(0xffffffffu, old, leader) >> sh16) & 0xFFFFu;
-        const uint32_t r = base + below;
+        r = base + below;
+        }
 #ifdef B2S_ABLATE_SCATTER
         if (valid && r == 0x7fffffff) {
 #else
@@ -701,7 +716,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                                                dxor, nd);
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __restrict__ plan,
                                                                  RadixCounters* __restrict__ ctr,
                                                                  int slot, uint64_t n,
@@ -815,16 +830,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
                 parity ^= 1u << cur;
                 B2S_PHASE(0);
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, RANK>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, RANK>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, RANK>(
                 claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
                 nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
         }
@@ -982,19 +997,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
             if (tma) {
                 mbar_wait(smem_addr(&s_mbar3[cur]), (parity >> cur) & 1u);
                 parity ^= 1u << cur;
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true, 0>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
                     lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true, 0>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
                     lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             }
             prev_valid = TILE;
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true, 0>(
                 noop, write_prev, s_gbase2[gcur], tile, (uint32_t)rem, tile_base, src, dst, vsrc,
                 vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                 prof_t);
@@ -1043,13 +1058,13 @@ int onesweep_cfg() {
     return cfg;
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
-b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
-                             void* lb) {
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
+b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
+                               void* lb) {
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
     constexpr size_t SMEM = SM::bytes;
-    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB>;
+    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>;
     static int occ = -1;  // per instantiation, per process (single device type)
     if (occ < 0) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1071,6 +1086,14 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
     }
     ctx->ev_pass[slots] = record(ctx);
     return B2S_OK;
+}
+
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
+                             void* lb) {
+    if (ctx->atomic_rank)
+        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb);
+    return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
@@ -1188,7 +1211,49 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     return B2S_OK;
 }
 
+// Checks the property the atomic ranking relies on: lanes of one warp
+// instruction adding to the same shared counter get old values in ascending
+// lane order. Every warp keeps private counters; digit patterns run from one
+// bin (all lanes collide) to 256 bins.
+__global__ void probe_lane_order_kernel(int iters, unsigned long long* bad) {
+    __shared__ uint32_t cnt[8][kRadix / 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t x = 0x9E3779B9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
+    unsigned long long nb = 0;
+    for (int it = 0; it < iters; ++it) {
+        for (int i = lane; i < kRadix / 2; i += 32) cnt[warp][i] = 0;
+        __syncwarp();
+        x ^= x << 13;
+        x ^= x >> 17;
+        x ^= x << 5;
+        const uint32_t bins = 1u << (it % 9);
+        const uint32_t d = (x >> 8) % bins;
+        const uint32_t sh16 = 16 * (d & 1);
+        const uint32_t r = (atomicAdd(&cnt[warp][d >> 1], 1u << sh16) >> sh16) & 0xFFFFu;
+        const uint32_t peers = match_digit<8>(d);
+        nb += (r != (uint32_t)__popc(peers & ((1u << lane) - 1u)));
+        __syncwarp();
+    }
+    if (nb) atomicAdd(bad, nb);
+}
+
 }  // namespace
+
+b2s_status probe_lane_order(b2s_ctx* ctx, bool* ok) {
+    *ok = false;
+    const char* e = getenv("B2S_RANK");
+    if (e && std::string(e) == "ballot") return B2S_OK;  // forced off
+    B2S_TRY(ctx->misc.ensure(64));
+    unsigned long long* bad = static_cast<unsigned long long*>(ctx->misc.ptr);
+    B2S_CUDA(cudaMemsetAsync(bad, 0, 8, ctx->stream));
+    probe_lane_order_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(288, bad);
+    B2S_LAUNCHED();
+    unsigned long long h = 1;
+    B2S_CUDA(cudaMemcpyAsync(&h, bad, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    *ok = h == 0;
+    return B2S_OK;
+}
 
 #ifdef B2S_PHASE_PROFILE
 extern "C" int b2s_debug_phase_cycles(unsigned long long* out16, int reset) {
