@@ -584,6 +584,33 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // ranks are stable. The highest lane of each digit group claims the group's
     // slots with one atomic and shuffles the base to its peers.
     const uint32_t lanemask_lt = (1u << lane) - 1u;
+    if constexpr (RANK == 1 && FULL) {
+        // atomic ranking in batches of 4 items: the batch's atomics are
+        // independent (the warp's shared accesses stay in program order, so
+        // the counters advance exactly as item by item) and their latencies
+        // overlap before the scatters consume them
+        constexpr int B = 4;
+#pragma unroll
+        for (int j0 = 0; j0 < ITEMS; j0 += B) {
+            uint32_t old[B], s16[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (j0 + b < ITEMS) {
+                    const uint32_t d = digit_of(keys[j0 + b], shift, dxor);
+                    s16[b] = 16 * (d & 1);
+                    old[b] = atom_add_shared(cnt_a + 4 * (d >> 1), 1u << s16[b]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (j0 + b < ITEMS) {
+                    const uint32_t r = (old[b] >> s16[b]) & 0xFFFFu;
+                    sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j0 + b]);
+                    if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j0 + b]);
+                }
+            }
+        }
+    } else
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const bool valid = FULL || (wbase + j * 32 + lane < tile_valid);
@@ -815,11 +842,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         // claim the next tile and stream it in during this tile's write-out
         // (by a thread that sits out the look-back)
         auto noop = []() {};
+        // the next tile id is fetched now (its atomic's latency hides behind
+        // this tile) but published and prefetched only after the look-back
+        uint32_t next_t = 0;
+        if (tid == THREADS - 1) next_t = atomicAdd(&plan->tile_counter[slot], 1u);
         auto claim = [&]() {
             if (tid == THREADS - 1) {
-                const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-                sh.tile[cur ^ 1] = t;
-                prefetch(t, cur ^ 1);
+                sh.tile[cur ^ 1] = next_t;
+                prefetch(next_t, cur ^ 1);
             }
         };
         const uint64_t tile_base = (uint64_t)tile * TILE;
@@ -874,7 +904,7 @@ struct PipeSmem {
     static constexpr size_t bytes = kCnt + 3 * kKeys + 3 * kVals + kMatch + kEarly;
 };
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
 __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan* __restrict__ plan,
                                                                       RadixCounters* __restrict__ ctr,
                                                                       int slot, uint64_t n,
@@ -997,19 +1027,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
             if (tma) {
                 mbar_wait(smem_addr(&s_mbar3[cur]), (parity >> cur) & 1u);
                 parity ^= 1u << cur;
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true, 0>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true, RANK>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
                     lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true, 0>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true, RANK>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
                     lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             }
             prev_valid = TILE;
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true, 0>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true, RANK>(
                 noop, write_prev, s_gbase2[gcur], tile, (uint32_t)rem, tile_base, src, dst, vsrc,
                 vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                 prof_t);
@@ -1096,12 +1126,12 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
     return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
-b2s_status launch_pipe_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
+b2s_status launch_pipe_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
     using SM = PipeSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
     constexpr size_t SMEM = SM::bytes;
-    auto kern = onesweep_pipe_kernel<U, VALS, LB, THREADS, ITEMS, MINB>;
+    auto kern = onesweep_pipe_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>;
     static int occ = -1;
     if (occ < 0) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
@@ -1122,6 +1152,13 @@ b2s_status launch_pipe_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, ui
     }
     ctx->ev_pass[slots] = record(ctx);
     return B2S_OK;
+}
+
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
+b2s_status launch_pipe_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
+    if (ctx->atomic_rank)
+        return launch_pipe_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb);
+    return launch_pipe_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 
 // smallest tile over all configurations: sizes the look-back scratch
