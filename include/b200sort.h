@@ -97,6 +97,16 @@ int b2s_device_count(void);
 b2s_status b2s_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* keys_in, void* keys_out,
                     const uint32_t* vals_in, uint32_t* vals_out, uint64_t n, uint32_t flags);
 
+/* Sorts `count` independent host arrays of n keys each (B2S_HOST only):
+ * keys_in[i] -> keys_out[i] (and optional payloads). The host->device copy of
+ * array i+1, the sort of array i and the device->host copy of array i-1 run
+ * concurrently on three streams (PCIe is full duplex), so a stream of batches
+ * is bounded by the slower copy direction, not by copy + sort + copy. Pinned
+ * host memory is required for the overlap. Synchronous. */
+b2s_status b2s_sort_batch(b2s_ctx* ctx, b2s_dtype dtype, const void* const* keys_in,
+                          void* const* keys_out, const uint32_t* const* vals_in,
+                          uint32_t* const* vals_out, uint64_t n, int count, uint32_t flags);
+
 /* ---- k-way merge ---------------------------------------------------------
  * Replaces the odd-even merge_split phases + rank-order gather of the root
  * merge (P/src/parallel_sort.cpp:59-134,217-248): merges k sorted runs into

@@ -293,6 +293,72 @@ b2s_status b2s_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* keys_in, void* ke
     return B2S_OK;
 }
 
+b2s_status b2s_sort_batch(b2s_ctx* ctx, b2s_dtype dtype, const void* const* keys_in,
+                          void* const* keys_out, const uint32_t* const* vals_in,
+                          uint32_t* const* vals_out, uint64_t n, int count, uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (!(flags & B2S_HOST)) return set_error(B2S_EINVAL, "b2s_sort_batch takes host buffers");
+    if (count < 0) return set_error(B2S_EINVAL, "negative batch count");
+    if ((vals_in == nullptr) != (vals_out == nullptr))
+        return set_error(B2S_EINVAL, "vals_in and vals_out must both be set or both be NULL");
+    if (count > 0 && (keys_in == nullptr || keys_out == nullptr))
+        return set_error(B2S_EINVAL, "null batch arrays");
+    timing_reset(ctx);
+    if (count == 0 || n == 0) return B2S_OK;
+    const bool with_vals = vals_in != nullptr;
+    const size_t kb = (size_t)key_bytes(dtype) * n, vb = 4 * n;
+    // two device stages; stage b holds array i (i % 2 == b) from its upload
+    // to the end of its download
+    B2S_TRY(ctx->stage_in.ensure(2 * kb));
+    if (with_vals) B2S_TRY(ctx->stage_vin.ensure(2 * vb));
+    cudaStream_t comp = ctx->stream;
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t ev_up[2] = {}, ev_sorted[2] = {}, ev_down[2] = {};
+    b2s_status st = B2S_OK;
+    cudaError_t e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&ev_up[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_sorted[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_down[b], cudaEventDisableTiming);
+    }
+    for (int i = 0; i < count && e == cudaSuccess && st == B2S_OK; ++i) {
+        const int b = i & 1;
+        char* dk = static_cast<char*>(ctx->stage_in.ptr) + b * kb;
+        uint32_t* dv = with_vals ? static_cast<uint32_t*>(ctx->stage_vin.ptr) + b * n : nullptr;
+        if (i >= 2) e = cudaStreamWaitEvent(up, ev_down[b], 0);  // stage b downloaded
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dk, keys_in[i], kb, cudaMemcpyHostToDevice, up);
+        if (e == cudaSuccess && with_vals)
+            e = cudaMemcpyAsync(dv, vals_in[i], vb, cudaMemcpyHostToDevice, up);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_up[b], up);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, ev_up[b], 0);
+        if (e != cudaSuccess) break;
+        st = radix_sort(ctx, dtype, dk, dk, dv, dv, n);
+        if (st != B2S_OK) break;
+        e = cudaEventRecord(ev_sorted[b], comp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(down, ev_sorted[b], 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(keys_out[i], dk, kb, cudaMemcpyDeviceToHost, down);
+        if (e == cudaSuccess && with_vals)
+            e = cudaMemcpyAsync(vals_out[i], dv, vb, cudaMemcpyDeviceToHost, down);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_down[b], down);
+    }
+    if (e != cudaSuccess && st == B2S_OK)
+        st = set_error(B2S_ECUDA, "b2s_sort_batch: %s", cudaGetErrorString(e));
+    if (down) cudaStreamSynchronize(down);
+    if (up) cudaStreamSynchronize(up);
+    cudaStreamSynchronize(comp);
+    for (int b = 0; b < 2; ++b) {
+        if (ev_up[b]) cudaEventDestroy(ev_up[b]);
+        if (ev_sorted[b]) cudaEventDestroy(ev_sorted[b]);
+        if (ev_down[b]) cudaEventDestroy(ev_down[b]);
+    }
+    if (up) cudaStreamDestroy(up);
+    if (down) cudaStreamDestroy(down);
+    if (st == B2S_OK) ctx->have_sort = true;
+    return st;
+}
+
 b2s_status b2s_merge(b2s_ctx* ctx, b2s_dtype dtype, const void* const* runs,
                      const uint32_t* const* run_vals, const uint64_t* lens, int k, void* out,
                      uint32_t* out_vals, uint32_t flags) {

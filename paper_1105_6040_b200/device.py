@@ -144,6 +144,28 @@ class Context:
                              _ptr(vals_out), _numel(keys), B2S_HOST if host else B2S_DEVICE))
         return out, vals_out
 
+    def sort_batch(self, keys_list, outs=None, vals_list=None, vals_outs=None):
+        """Sorts a list of equally sized host (numpy) arrays with the uploads,
+        sorts and downloads of consecutive arrays overlapped (b2s_sort_batch)."""
+        if not keys_list:
+            return [], None
+        n = _numel(keys_list[0])
+        code = dtype_code(keys_list[0])
+        for x in keys_list:
+            if not _is_host(x) or _numel(x) != n or dtype_code(x) != code:
+                raise ValueError("sort_batch takes equally sized host arrays of one dtype")
+        if outs is None:
+            outs = [np.empty_like(x) for x in keys_list]
+        if vals_list is not None and vals_outs is None:
+            vals_outs = [np.empty_like(v) for v in vals_list]
+        c = len(keys_list)
+        ki = (ctypes.c_void_p * c)(*[_ptr(x) for x in keys_list])
+        ko = (ctypes.c_void_p * c)(*[_ptr(x) for x in outs])
+        vi = (ctypes.c_void_p * c)(*[_ptr(v) for v in vals_list]) if vals_list is not None else None
+        vo = (ctypes.c_void_p * c)(*[_ptr(v) for v in vals_outs]) if vals_outs is not None else None
+        check(lib().b2s_sort_batch(self._h, code, ki, ko, vi, vo, n, c, B2S_HOST))
+        return outs, vals_outs
+
     def partitioned_sort(self, keys, p: int, out=None, vals=None, vals_out=None, stream=None):
         """scatter / local sort / merge on this device with p partitions."""
         _check_1d(keys, "keys")

@@ -193,3 +193,20 @@ def test_check_sorted_fingerprint_matches_oracle(ctx):
         inv, fp, _ = ctx.check_sorted(to_dev(x))
         assert fp == oracle.fingerprint(x)
         assert inv == int(np.sum(x[1:] < x[:-1]))
+
+
+def test_sort_batch_host_pipeline(ctx):
+    """b2s_sort_batch: overlapped upload / sort / download of several host arrays."""
+    rng = np.random.default_rng(21)
+    for dt in DTYPES:
+        n = 300_001
+        batch = [rand_keys(n, dt, rng, kind) for kind in ("uniform", "dups", "topbyte", "equal", "uniform")]
+        outs, _ = ctx.sort_batch(batch)
+        for x, o in zip(batch, outs):
+            assert np.array_equal(o, oracle.sort(x))
+    keys = [rand_keys(100_000, np.uint64, rng, "dups") for _ in range(3)]
+    vals = [np.arange(100_000, dtype=np.uint32) for _ in range(3)]
+    ok, ov = ctx.sort_batch(keys, vals_list=vals)
+    for k, v, a, b in zip(keys, vals, ok, ov):
+        ek, ev = oracle.stable_sort_kv(k, v)
+        assert np.array_equal(a, ek) and np.array_equal(b, ev)
