@@ -15,8 +15,10 @@ from paper_1105_6040_b200.device import Context  # noqa: E402
 DTYPES = [np.int32, np.uint32, np.int64, np.uint64]
 TORCH = {np.int32: torch.int32, np.uint32: torch.uint32, np.int64: torch.int64,
          np.uint64: torch.uint64}
-SIZES = [0, 1, 2, 31, 1000, 3071, 3072, 4095, 4096, 4097, 6143, 6144, 8191, 8192, 8193,
-         100_000, (1 << 20) + 7]
+# tile edges of every configuration: 512x20 (u32), 512x10 (u32+payload),
+# 512x8 (u64), 512x6 (u64+payload), plus look-back word width edges elsewhere
+SIZES = [0, 1, 2, 31, 1000, 3071, 3072, 3073, 4095, 4096, 4097, 5119, 5120, 5121, 8191, 8192,
+         8193, 10239, 10240, 10241, 20480, 20481, 100_000, (1 << 20) + 7]
 
 
 @pytest.fixture(scope="module")
@@ -108,9 +110,9 @@ def test_sort_in_place_and_host_buffers(ctx, dt):
 
 @pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("kind", ["dups", "uniform", "equal"])
-def test_sort_pairs_stable(ctx, dt, kind):
+@pytest.mark.parametrize("n", [123_457, 3072, 5121, 1])
+def test_sort_pairs_stable(ctx, dt, kind, n):
     rng = np.random.default_rng(17)
-    n = 123_457
     keys = rand_keys(n, dt, rng, kind)
     vals = np.arange(n, dtype=np.uint32)
     ek, ev = oracle.stable_sort_kv(keys, vals)
@@ -210,3 +212,16 @@ def test_sort_batch_host_pipeline(ctx):
     for k, v, a, b in zip(keys, vals, ok, ov):
         ek, ev = oracle.stable_sort_kv(k, v)
         assert np.array_equal(a, ek) and np.array_equal(b, ev)
+
+
+def test_n_at_least_2p30_uses_64bit_lookback(ctx):
+    """n >= 2^30 switches the look-back words to 64 bits (a digit's prefix no
+    longer fits 30 bits); sortedness + multiset equality at 2^30 + 12345."""
+    n = (1 << 30) + 12345
+    keys = ctx.gen_keys(n, 5, torch.int32, shift=32)
+    _, _, ms_in = ctx.check_sorted(keys)
+    out, _ = ctx.sort(keys)
+    inv, _, ms_out = ctx.check_sorted(out)
+    assert inv == 0 and ms_in == ms_out
+    del keys, out
+    torch.cuda.empty_cache()
