@@ -1058,6 +1058,349 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
         atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised onesweep: warps 0-7 ("rankers") load, count, publish and
+// rank tile k while warps 8-15 ("writers") resolve tile k-1's look-back and
+// write it out, then refill its buffer with a TMA copy of a new tile. Three
+// tile buffers rotate; the groups hand tiles over with mbarriers and sync
+// internally with named barriers, so the look-back latency and the write-out
+// of one tile overlap the ranking of the next.
+
+__device__ __forceinline__ void named_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+constexpr int kWsSlots = 3;
+constexpr uint32_t kWsEnd = 0xFFFFFFFFu;
+
+template <typename U, bool VALS, int ITEMS>
+struct WsSmem {
+    static constexpr int TILE = 256 * ITEMS;  // ranked by 256 threads
+    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);
+    static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
+    static constexpr size_t kCnt = 8 * (kRadix / 2) * 4;   // rankers' packed counters
+    static constexpr size_t kEarly = 8 * kRadix * 4;       // rankers' early counts
+    static constexpr size_t bytes = kWsSlots * (kKeys + kVals) + kCnt + kEarly;
+};
+
+template <typename LB>
+struct WsShared {
+    using OFF = LB;
+    OFF goff[kRadix];
+    OFF gbase[kRadix];             // writers only
+    uint32_t start[2][kRadix];     // per tile parity: digit starts in the tile
+    uint32_t nhist[kRadix];
+    uint32_t wsum[8];
+    unsigned long long wsum64[kRadix / 32];
+    uint32_t slot_tile[kWsSlots];
+    uint32_t slot_valid[kWsSlots];
+    uint32_t slot_tma[kWsSlots];
+    uint32_t staged_tile[2];
+    uint32_t staged_valid[2];
+    uint32_t dummy[32];
+    alignas(8) unsigned long long full[kWsSlots];  // slot landed / set (writer -> ranker)
+    alignas(8) unsigned long long staged[2];       // tile ranked + staged (ranker -> writer)
+    alignas(8) unsigned long long statefree[2];    // start[] of a parity free (writer -> ranker)
+};
+
+template <typename U, bool VALS, typename LB, int ITEMS>
+__global__ void __launch_bounds__(512, 2) onesweep_ws_kernel(RadixPlan* __restrict__ plan,
+                                                             RadixCounters* __restrict__ ctr,
+                                                             int slot, uint64_t n, uint32_t ntiles,
+                                                             LB* __restrict__ lb_cur,
+                                                             LB* __restrict__ lb_next) {
+    using SM = WsSmem<U, VALS, ITEMS>;
+    using W = LookbackWord<LB>;
+    using OFF = LB;
+    constexpr int TILE = SM::TILE;
+    constexpr int HALF = kRadix / 2;
+    constexpr int WSEG = 32 * ITEMS;
+    static_assert(TILE < 65536, "packed 16-bit warp counters");
+
+    const int na = plan->num_active;
+    if (slot >= na) return;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    U* kbuf[kWsSlots];
+    uint32_t* vbuf[kWsSlots];
+#pragma unroll
+    for (int b = 0; b < kWsSlots; ++b) {
+        kbuf[b] = reinterpret_cast<U*>(smem + b * SM::kKeys);
+        vbuf[b] = reinterpret_cast<uint32_t*>(smem + kWsSlots * SM::kKeys + b * SM::kVals);
+    }
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kWsSlots * (SM::kKeys + SM::kVals));
+    uint32_t* s_early = s_cnt + SM::kCnt / 4;
+    __shared__ WsShared<LB> sh;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const bool ranker = warp < 8;
+    const int shift = 8 * plan->digit[slot];
+    const uint32_t dxor = plan->dxor[slot];
+    const U* src = static_cast<const U*>(plan->ksrc[slot]);
+    U* dst = static_cast<U*>(plan->kdst[slot]);
+    const uint32_t* vsrc = plan->vsrc[slot];
+    uint32_t* vdst = plan->vdst[slot];
+    const bool nd_on = slot + 1 < na;
+    const int nd_shift = nd_on ? 8 * plan->digit[slot + 1] : 0;
+    const uint32_t nd_dxor = nd_on ? plan->dxor[slot + 1] : 0u;
+    const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
+                     (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
+    const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
+
+    // claim a tile into slot b and start its copy (one writer thread)
+    auto fill = [&](int b) {
+        const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
+        const uint32_t mb = smem_addr(&sh.full[b]);
+        if (t >= ntiles) {
+            sh.slot_tile[b] = kWsEnd;
+            mbar_arrive(mb);
+            return;
+        }
+        const uint64_t rem = n - (uint64_t)t * TILE;
+        const uint32_t valid = rem < (uint64_t)TILE ? (uint32_t)rem : (uint32_t)TILE;
+        sh.slot_tile[b] = t;
+        sh.slot_valid[b] = valid;
+        const bool use_tma = tma && valid == (uint32_t)TILE;
+        sh.slot_tma[b] = use_tma;
+        if (use_tma) {
+            fence_proxy_async();
+            mbar_expect_tx(mb, tx_bytes);
+            bulk_g2s(smem_addr(kbuf[b]), src + (uint64_t)t * TILE, (uint32_t)SM::kKeys, mb);
+            if constexpr (VALS)
+                bulk_g2s(smem_addr(vbuf[b]), vsrc + (uint64_t)t * TILE, (uint32_t)SM::kVals, mb);
+        } else {
+            mbar_arrive(mb);
+        }
+    };
+
+    // setup: digit offsets, counters, barriers, first fills
+    if (tid < kRadix) {
+        const unsigned long long c = plan->hist[slot][tid];
+        unsigned long long incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) sh.wsum64[tid >> 5] = incl;
+        sh.goff[tid] = (OFF)(incl - c);
+        sh.nhist[tid] = 0;
+    }
+    for (int i = tid; i < 8 * HALF; i += 512) s_cnt[i] = 0;
+    for (int i = tid; i < 8 * kRadix; i += 512) s_early[i] = 0;
+    if (tid == 0) {
+        for (int b = 0; b < kWsSlots; ++b) mbar_init(smem_addr(&sh.full[b]), 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(smem_addr(&sh.staged[b]), 1);
+            mbar_init(smem_addr(&sh.statefree[b]), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < kRadix) {
+        unsigned long long base = 0;
+#pragma unroll
+        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? sh.wsum64[w] : 0ull;
+        sh.goff[tid] += (OFF)base;
+    }
+    if (tid == 256)
+        for (int b = 0; b < kWsSlots; ++b) fill(b);
+    __syncthreads();
+
+    if (ranker) {
+        // ------------------------------------------------------------ rankers
+        const uint32_t cnt_a = smem_addr(s_cnt + warp * HALF);
+        uint32_t* ecnt = s_early + warp * kRadix;
+        const uint32_t dummy_a = smem_addr(sh.dummy + lane);
+        uint32_t ph_full = 0, ph_free = 0;
+        for (uint32_t k = 0;; ++k) {
+            const int s = (int)(k % kWsSlots);
+            const int b = (int)(k & 1);
+            mbar_wait(smem_addr(&sh.full[s]), (ph_full >> s) & 1u);
+            ph_full ^= 1u << s;
+            const uint32_t tile = sh.slot_tile[s];
+            if (tile == kWsEnd) {
+                if (tid == 0) {
+                    sh.staged_tile[b] = kWsEnd;
+                    mbar_arrive(smem_addr(&sh.staged[b]));
+                }
+                break;
+            }
+            if (k >= 2) {  // the writers are done with start[b] of tile k-2
+                mbar_wait(smem_addr(&sh.statefree[b]), (ph_free >> b) & 1u);
+                ph_free ^= 1u << b;
+            }
+            const uint32_t valid = sh.slot_valid[s];
+            const bool full = valid == (uint32_t)TILE;
+            const bool from_smem = sh.slot_tma[s] != 0;
+            const uint64_t tile_base = (uint64_t)tile * TILE;
+            if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
+            U* kb = kbuf[s];
+            uint32_t* vb = vbuf[s];
+            const uint32_t wbase = warp * WSEG;
+            U keys[ITEMS];
+            uint32_t vals[VALS ? ITEMS : 1];
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t idx = wbase + j * 32 + lane;
+                if (from_smem) {
+                    keys[j] = kb[idx];
+                    if constexpr (VALS) vals[j] = vb[idx];
+                } else {
+                    keys[j] = idx < valid ? src[tile_base + idx] : U(0);
+                    if constexpr (VALS) vals[j] = idx < valid ? vsrc[tile_base + idx] : 0u;
+                }
+            }
+            // early counts
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t d = digit_of(keys[j], shift, dxor);
+                if (full || wbase + j * 32 + lane < valid)
+                    atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
+            }
+            named_bar(1, 256);
+            // digit pairs: prefix over the 8 ranker warps, publish aggregates
+            uint32_t pair = 0;
+            if (tid < HALF) {
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    uint32_t* e = s_early + w * kRadix;
+                    const uint32_t c = e[tid] | (e[HALF + tid] << 16);
+                    e[tid] = 0;
+                    e[HALF + tid] = 0;
+                    s_cnt[w * HALF + tid] = pair;
+                    pair += c;
+                }
+                const uint32_t c0 = pair & 0xFFFFu, c1 = pair >> 16;
+                LB* slotp = lb_cur + (size_t)tile * kRadix + 2 * tid;
+                const LB flag = tile == 0 ? W::kInc : W::kAgg;
+                st_relaxed(slotp, flag | (LB)c0);
+                st_relaxed(slotp + 1, flag | (LB)c1);
+                uint32_t incl = c0 + c1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (lane == 31) sh.wsum[warp] = incl;
+                sh.start[b][2 * tid] = incl - c0 - c1;
+                sh.start[b][2 * tid + 1] = incl - c1;
+            }
+            named_bar(1, 256);
+            if (tid < HALF) {
+                uint32_t base = 0;
+#pragma unroll
+                for (int w = 0; w < HALF / 32; ++w) base += (w < warp) ? sh.wsum[w] : 0u;
+                const uint32_t s0 = sh.start[b][2 * tid] + base, s1 = sh.start[b][2 * tid + 1] + base;
+                sh.start[b][2 * tid] = s0;
+                sh.start[b][2 * tid + 1] = s1;
+                const uint32_t add = s0 | (s1 << 16);
+#pragma unroll
+                for (int w = 0; w < 8; ++w) s_cnt[w * HALF + tid] += add;
+            }
+            named_bar(1, 256);
+            // rank (lane-ordered atomics) and stage in place
+            const uint32_t keys_a = smem_addr(kb), vals_a = smem_addr(vb);
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const bool ok = full || wbase + j * 32 + lane < valid;
+                const uint32_t d = digit_of(keys[j], shift, dxor);
+                const uint32_t s16 = 16 * (d & 1);
+                const uint32_t old = atom_add_shared(ok ? cnt_a + 4 * (d >> 1) : dummy_a,
+                                                     ok ? 1u << s16 : 0u);
+                const uint32_t r = (old >> s16) & 0xFFFFu;
+                if (ok) {
+                    sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j]);
+                    if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j]);
+                }
+            }
+#pragma unroll
+            for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
+            named_bar(1, 256);
+            if (tid == 0) {
+                sh.staged_tile[b] = tile;
+                sh.staged_valid[b] = valid;
+                mbar_arrive(smem_addr(&sh.staged[b]));
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ writers
+        const int wt = tid - 256;  // 0..255: one digit each for the look-back
+        uint32_t ph_staged = 0;
+        for (uint32_t k = 0;; ++k) {
+            const int s = (int)(k % kWsSlots);
+            const int b = (int)(k & 1);
+            mbar_wait(smem_addr(&sh.staged[b]), (ph_staged >> b) & 1u);
+            ph_staged ^= 1u << b;
+            const uint32_t tile = sh.staged_tile[b];
+            if (tile == kWsEnd) break;
+            const uint32_t valid = sh.staged_valid[b];
+            // look-back for digit wt
+            {
+                const uint32_t st0 = sh.start[b][wt];
+                const uint32_t mycount = (wt + 1 < kRadix ? sh.start[b][wt + 1] : valid) - st0;
+                unsigned long long excl = 0;
+                if (tile > 0) {
+                    int64_t pred = (int64_t)tile - 1;
+                    bool done = false;
+                    const LB* col = lb_cur + wt;
+                    LB* mine = lb_cur + (size_t)tile * kRadix + wt;
+                    while (__any_sync(0xffffffffu, !done)) {
+                        if (!done) {
+                            LB w[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * kRadix) : W::kInc;
+                            bool stop = false;
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const LB f = W::flag(w[i]);
+                                if (!stop && f != 0) {
+                                    excl += (unsigned long long)(w[i] & W::kMask);
+                                    done = (f == 2);
+                                    stop = done;
+                                    pred -= done ? 0 : 1;
+                                } else {
+                                    stop = true;
+                                }
+                            }
+                            if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
+                        }
+                    }
+                }
+                sh.gbase[wt] = (OFF)(sh.goff[wt] + excl - st0);
+            }
+            named_bar(2, 256);
+            if (wt == 0) mbar_arrive(smem_addr(&sh.statefree[b]));  // start[b] no longer read
+            // write out the staged tile from slot s
+            const U* kb = kbuf[s];
+            const uint32_t* vb = vbuf[s];
+            const bool full = valid == (uint32_t)TILE;
+#pragma unroll 4
+            for (int j = 0; j < ITEMS; ++j) {
+                const uint32_t i = j * 256 + wt;
+                if (full || i < valid) {
+                    const U key = kb[i];
+                    const OFF g = sh.gbase[digit_of(key, shift, dxor)] + (OFF)i;
+                    __stcs(dst + g, key);
+                    if constexpr (VALS) __stcs(vdst + g, vb[i]);
+                    if (nd_on) atomicAdd(sh.nhist + digit_of(key, nd_shift, nd_dxor), 1u);
+                }
+            }
+            named_bar(2, 256);
+            if (wt == 0) fill(s);  // slot s is free: claim the next tile into it
+        }
+        named_bar(2, 256);
+        if (nd_on && wt < kRadix && sh.nhist[wt])
+            atomicAdd(&ctr->hist[slot + 1][wt], (unsigned long long)sh.nhist[wt]);
+    }
+}
+
 template <typename U>
 __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n, int with_vals) {
     if (!plan->do_copy) return;
@@ -1161,6 +1504,34 @@ b2s_status launch_pipe_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, ui
     return launch_pipe_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 
+template <typename U, bool VALS, typename LB, int ITEMS>
+b2s_status launch_ws_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
+    using SM = WsSmem<U, VALS, ITEMS>;
+    constexpr int TILE = SM::TILE;
+    constexpr size_t SMEM = SM::bytes;
+    auto kern = onesweep_ws_kernel<U, VALS, LB, ITEMS>;
+    static int occ = -1;
+    if (occ < 0) {
+        B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+        int o = 0;
+        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 512, SMEM));
+        occ = o > 0 ? o : 1;
+    }
+    const uint64_t ntiles64 = (n + TILE - 1) / TILE;
+    const uint32_t ntiles = (uint32_t)ntiles64;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ * ctx->num_sms);
+    LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
+    const int slots = (int)sizeof(U);
+    for (int s = 0; s < slots; ++s) {
+        ctx->ev_pass[s] = record(ctx);
+        kern<<<grid, 512, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
+                                               region[(s + 1) & 1]);
+        B2S_LAUNCHED();
+    }
+    ctx->ev_pass[slots] = record(ctx);
+    return B2S_OK;
+}
+
 // smallest tile over all configurations: sizes the look-back scratch
 constexpr int kMinTile = 512 * 6;  // smallest tile of any configuration
 
@@ -1175,6 +1546,9 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
         if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 18, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 9 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 24>(ctx, plan, ctr, n, lb);
+        if (cfg == 10 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 20>(ctx, plan, ctr, n, lb);
+        if (cfg == 11 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 28>(ctx, plan, ctr, n, lb);
         if (cfg == 6) return launch_pipe_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 7) return launch_pipe_cfg<U, VALS, LB, 512, 14, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 8) return launch_pipe_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
