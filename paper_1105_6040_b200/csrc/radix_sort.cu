@@ -33,6 +33,7 @@
 // 2 * (key_bytes + val_bytes) * n. The prologue reads key_bytes * n once.
 #include <cub/warp/warp_scan.cuh>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <string>
@@ -1445,6 +1446,12 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
         int o = 0;
         B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
         occ = o > 0 ? o : 1;
+        if (getenv("B2S_DEBUG")) {
+            cudaFuncAttributes fa;
+            cudaFuncGetAttributes(&fa, kern);
+            fprintf(stderr, "[b2s] onesweep<%zuB keys, vals=%d, %d thr, %d items, rank=%d>: dyn smem %zu + static %zu B, regs %d, %d CTA/SM\n",
+                    sizeof(U), (int)VALS, THREADS, ITEMS, RANK, (size_t)SMEM, (size_t)fa.sharedSizeBytes, fa.numRegs, occ);
+        }
     }
     const uint64_t ntiles64 = (n + TILE - 1) / TILE;
     const uint32_t ntiles = (uint32_t)ntiles64;
@@ -1560,7 +1567,8 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);
     } else {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 4>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
     }
 }
 
