@@ -284,14 +284,12 @@ struct OnesweepSmem {
     static constexpr size_t kCnt = (size_t)WARPS * (kRadix / 2) * 4;  // packed u16 pairs
     static constexpr size_t kKeys = (size_t)TILE * sizeof(U);         // one tile buffer
     static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
-    static constexpr size_t kMatch = MATCH_SMEM ? (size_t)WARPS * kRadix * 4 : 0;
-    // unpacked early counts; they share the match masks' space (both are all
-    // zero between uses: the digit section clears the counts, every ranking
-    // step clears its mask)
-    static constexpr size_t kEarly = MATCH_SMEM ? 0 : (size_t)WARPS * kRadix * 4;
-    // counters | keys[2] | vals[2] | match masks | early counts: tile i+1
-    // streams in by TMA while tile i is ranked in place in its own buffer
-    static constexpr size_t bytes = kCnt + 2 * kKeys + 2 * kVals + kMatch + kEarly;
+    // counters | keys[2] | vals[2]: tile i+1 streams in by TMA while tile i is
+    // ranked in place in its own buffer. The per-warp early counts and match
+    // masks (WARPS x 1 KB) live in the idle tile buffer until the next tile's
+    // copy is issued (after the look-back).
+    static constexpr size_t bytes = kCnt + 2 * kKeys + 2 * kVals;
+    static_assert(kKeys >= (size_t)WARPS * kRadix * 4, "idle tile buffer holds the early counts");
 };
 
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier ----------
@@ -515,6 +513,14 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // that hit the same counter); the digit section packs them into 16-bit
     // pairs for ranking.
     uint32_t* ecnt = s_early + warp * kRadix;
+    if constexpr (!PIPE) {
+        // the counts live in the idle tile buffer (nothing streams into it
+        // before this tile's look-back is done); each warp clears its own 1 KB
+        uint4* z = reinterpret_cast<uint4*>(ecnt);
+#pragma unroll
+        for (int i = lane; i < kRadix / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+        __syncwarp();
+    }
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t d = digit_of(keys[j], shift, dxor);
@@ -767,8 +773,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                          reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + SM::kVals)};
     __shared__ TileShared<LB> sh;
     __shared__ typename TileShared<LB>::OFF s_gbase[kRadix];
-    uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 2 * SM::kKeys + 2 * SM::kVals);
-    uint32_t* s_early = MATCH_SMEM ? s_match : s_match + SM::kMatch / 4;
 
     const int tid = threadIdx.x;
     const int shift = 8 * plan->digit[slot];
@@ -813,9 +817,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         sh.nhist[tid] = 0;
     }
     for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
-    for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_early[i] = 0;
-    if constexpr (MATCH_SMEM)
-        for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_match[i] = 0;
     if (tid == THREADS - 1) {
         mbar_init(mbar_a[0], 1);
         mbar_init(mbar_a[1], 1);
@@ -856,6 +857,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
         if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
+        uint32_t* idle = reinterpret_cast<uint32_t*>(kbuf[cur ^ 1]);
         if (rem >= (uint64_t)TILE) {
             if (tma) {
                 mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
@@ -863,16 +865,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 B2S_PHASE(0);
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, RANK>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
+                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, RANK>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
+                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t);
             }
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, RANK>(
                 claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
-                nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc, prof_t);
+                nd, s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t);
         }
         __syncthreads();
         B2S_PHASE(5);
@@ -1540,35 +1542,35 @@ b2s_status launch_ws_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
 }
 
 // smallest tile over all configurations: sizes the look-back scratch
-constexpr int kMinTile = 512 * 6;  // smallest tile of any configuration
+constexpr int kMinTile = 512 * 6;  // smallest tile of any configuration (u64 + payload, cfg 1)
 
 template <typename U, bool VALS, typename LB>
 b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
+    // Defaults fill the 2-CTA/SM shared-memory budget (two tile buffers of
+    // keys and payloads + 8 KB of counters per CTA); other configurations are
+    // tuning alternatives (B2S_ONESWEEP_CFG), kept with their measured results
+    // in DESIGN.md.
     const int cfg = onesweep_cfg();
-    if constexpr (sizeof(U) == 4 && VALS) {  // 8 B/pair in flight per item
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 3>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
+    if constexpr (sizeof(U) == 4 && VALS) {
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
         if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
-        if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 18, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 4) return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 22, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 9 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 24>(ctx, plan, ctr, n, lb);
         if (cfg == 10 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 20>(ctx, plan, ctr, n, lb);
-        if (cfg == 11 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 28>(ctx, plan, ctr, n, lb);
         if (cfg == 6) return launch_pipe_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 7) return launch_pipe_cfg<U, VALS, LB, 512, 14, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 8) return launch_pipe_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
-        // default: 10240-key tiles (measured best on B200: larger tiles amortise
-        // the per-tile 256-digit work; 22+ items spill)
-        return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 3>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
     } else {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 12, 4>(ctx, plan, ctr, n, lb);
-        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     }
 }
 
