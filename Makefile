@@ -42,6 +42,13 @@ $(LIB)/libb200sort_prof.so: $(SRC)/*.cu $(HDRS)
 lbexp:
 	for w in 0; do mkdir -p build/lb$$w; for f in $(CU); do $(NVCC) $(NVFLAGS) -DB2S_MATCH_HYBRID=$$w -c $(SRC)/$$f.cu -o build/lb$$w/$$f.o || exit 1; done; $(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_lb$$w.so $(addprefix build/lb$$w/,$(addsuffix .o,$(CU))) -lcudart; done
 
+# one experimental build of radix_sort.cu: make variant NAME=x DEFS="-DFOO=1"
+# -> lib/libb200sort_x.so (select with B2S_LIB)
+variant: $(OBJS)
+	@mkdir -p build/v_$(NAME)
+	$(NVCC) $(NVFLAGS) $(DEFS) -Xptxas -v -c $(SRC)/radix_sort.cu -o build/v_$(NAME)/radix_sort.o 2> build/v_$(NAME)/ptxas.txt || (cat build/v_$(NAME)/ptxas.txt; exit 1)
+	$(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_$(NAME).so build/v_$(NAME)/radix_sort.o $(filter-out $(OBJ)/radix_sort.o,$(OBJS)) -lcudart
+
 oracle:
 	bash oracle/build_ref.sh
 

@@ -420,7 +420,7 @@ struct TileShared {
 // Write-out of a staged tile: runs of equal digits go to consecutive global
 // slots (consecutive threads, consecutive positions); the next slot's digit is
 // counted on the way out.
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool AGG = false>
 __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbuf,
                                               const typename TileShared<LB>::OFF* gbase,
                                               uint32_t tile_valid, U* __restrict__ dst,
@@ -440,7 +440,19 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
             __stcs(dst + g, k);
             if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
 #ifndef B2S_ABLATE_NEXTHIST
-            if (nd.on) atomicAdd(nd.hist + digit_of(k, nd.shift, nd.dxor), 1u);  // ATOMS.POPC.INC
+            if (nd.on) {
+                const uint32_t dn = digit_of(k, nd.shift, nd.dxor);
+                if (AGG && full) {
+                    // skewed pass: lanes sharing lane 0's next digit count it
+                    // with one add (same-address atomics serialise)
+                    const uint32_t d0 = __shfl_sync(0xffffffffu, dn, 0);
+                    const uint32_t m = __ballot_sync(0xffffffffu, dn == d0);
+                    if (dn != d0) atomicAdd(nd.hist + dn, 1u);
+                    else if ((threadIdx.x & 31) == 0) atomicAdd(nd.hist + d0, (uint32_t)__popc(m));
+                } else {
+                    atomicAdd(nd.hist + dn, 1u);  // ATOMS.POPC.INC
+                }
+            }
 #endif
         }
     }
@@ -459,9 +471,13 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                                               uint32_t* s_match, uint32_t* s_early,
                                               TileShared<LB>& sh,
                                               unsigned long long* prof_acc,
-                                              long long& prof_t) {
+                                              long long& prof_t, uint32_t hot = 0) {
+    // RANK: 0 ballot matching, 1 lane-ordered atomics, 2 atomics except for
+    // the pass's hot digit, whose lanes are counted and ranked by one ballot
+    // per row against a warp-uniform running count (skewed passes)
     (void)prof_acc;
     (void)prof_t;
+    (void)hot;
     using W = LookbackWord<LB>;
     using OFF = typename TileShared<LB>::OFF;
     constexpr int WARPS = THREADS / 32;
@@ -521,10 +537,23 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         for (int i = lane; i < kRadix / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
         __syncwarp();
     }
+    if constexpr (RANK == 2) {
+        uint32_t hot_n = 0;
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t d = digit_of(keys[j], shift, dxor);
-        if (FULL || wbase + j * 32 + lane < tile_valid) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t d = digit_of(keys[j], shift, dxor);
+            const bool valid = FULL || wbase + j * 32 + lane < tile_valid;
+            const bool is_hot = valid && d == hot;
+            hot_n += __popc(__ballot_sync(0xffffffffu, is_hot));
+            if (valid && !is_hot) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
+        }
+        if (lane == 0 && hot_n) atomicAdd(ecnt + ((hot & 1) * HALF + (hot >> 1)), hot_n);
+    } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t d = digit_of(keys[j], shift, dxor);
+            if (FULL || wbase + j * 32 + lane < tile_valid) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
+        }
     }
     __syncthreads();  // also: every warp has read its keys out of kbuf
     B2S_PHASE(1);
@@ -591,7 +620,37 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // ranks are stable. The highest lane of each digit group claims the group's
     // slots with one atomic and shuffles the base to its peers.
     const uint32_t lanemask_lt = (1u << lane) - 1u;
-    if constexpr (RANK == 1 && FULL) {
+    if constexpr (RANK == 2 && FULL) {
+        // hot lanes: the warp's running offset of the hot digit (nobody
+        // else touches its counter) plus the lanes below in this row
+        uint32_t hot_run = (s_cnt[warp * HALF + (hot >> 1)] >> (16 * (hot & 1))) & 0xFFFFu;
+        constexpr int B = 4;
+#pragma unroll
+        for (int j0 = 0; j0 < ITEMS; j0 += B) {
+            uint32_t old[B], s16[B], r[B];
+            bool h[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (j0 + b < ITEMS) {
+                    const uint32_t d = digit_of(keys[j0 + b], shift, dxor);
+                    h[b] = d == hot;
+                    const uint32_t hm = __ballot_sync(0xffffffffu, h[b]);
+                    r[b] = hot_run + __popc(hm & lanemask_lt);
+                    hot_run += __popc(hm);
+                    s16[b] = 16 * (d & 1);
+                    old[b] = atom_add_shared_if(!h[b], cnt_a + 4 * (d >> 1), 1u << s16[b]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (j0 + b < ITEMS) {
+                    const uint32_t rr = h[b] ? r[b] : (old[b] >> s16[b]) & 0xFFFFu;
+                    sts_key(keys_a + rr * (uint32_t)sizeof(U), keys[j0 + b]);
+                    if constexpr (VALS) sts_key(vals_a + 4 * rr, vals[j0 + b]);
+                }
+            }
+        }
+    } else if constexpr (RANK == 1 && FULL) {
         // atomic ranking in batches of 4 items: the batch's atomics are
         // independent (the warp's shared accesses stay in program order, so
         // the counters advance exactly as item by item) and their latencies
@@ -626,7 +685,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         const uint32_t peers = 1u << lane;
 #else
         uint32_t r;
-        if constexpr (RANK == 1) {
+        if constexpr (RANK >= 1) {
             // lane-ordered shared atomics: lanes adding to the same counter in one
             // warp instruction receive old values in ascending lane order on this
             // device (verified at context creation by b2s::probe_lane_order), so
@@ -746,8 +805,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // ---- write runs of equal digits; clear this warp's counters
 #pragma unroll
     for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
-    writeout_tile<U, VALS, LB, THREADS, ITEMS>(kbuf, vbuf, gbase_out, tile_valid, dst, vdst, shift,
-                                               dxor, nd);
+    writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2>(kbuf, vbuf, gbase_out, tile_valid, dst, vdst,
+                                                          shift, dxor, nd);
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
@@ -756,14 +815,42 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                                                                  int slot, uint64_t n,
                                                                  uint32_t ntiles,
                                                                  LB* __restrict__ lb_cur,
-                                                                 LB* __restrict__ lb_next) {
+                                                                 LB* __restrict__ lb_next,
+                                                                 uint64_t skew_limit) {
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
     static_assert(THREADS >= kRadix, "one thread per digit is required");
     static_assert(TILE < 65536, "packed 16-bit warp counters");
+    // RANK: 0 ballots, 1 atomics; 2 atomics unless the pass is skewed, 3
+    // hot-digit ranking only if it is. Same-address shared atomics serialise
+    // across the lanes that share a digit, so in a pass with a hot digit (more
+    // than skew_limit keys) that digit is counted and ranked by ballots and
+    // the rest by atomics. 2 and 3 are launched back to back per pass, 3 as a
+    // programmatic dependent of 2: its CTAs take the SMs as 2's drain, and the
+    // one not suited to the pass exits at once. The histogram they decide on
+    // was final before 2 started.
+    constexpr int TR = RANK == 3 ? 2 : (RANK == 2 ? 1 : RANK);
+    if constexpr (RANK == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     const int na = plan->num_active;
     if (slot >= na) return;
+    const int tid = threadIdx.x;
+    unsigned long long c = 0;  // this thread's digit count of the pass
+    if (tid < kRadix) c = plan->hist[slot][tid];
+    uint32_t hot = 0;  // the pass's most frequent digit (RANK 3)
+    if constexpr (RANK >= 2) {
+        const bool skewed = __syncthreads_or(tid < kRadix && c > skew_limit) != 0;
+        if (skewed != (RANK == 3)) return;
+        if constexpr (RANK == 3) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            __shared__ unsigned long long s_hot;
+            if (tid == 0) s_hot = 0;
+            __syncthreads();
+            if (tid < kRadix) atomicMax(&s_hot, (c << 8) | (unsigned long long)tid);
+            __syncthreads();
+            hot = (uint32_t)(s_hot & 0xFF);
+        }
+    }
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);
@@ -774,7 +861,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     __shared__ TileShared<LB> sh;
     __shared__ typename TileShared<LB>::OFF s_gbase[kRadix];
 
-    const int tid = threadIdx.x;
     const int shift = 8 * plan->digit[slot];
     const uint32_t dxor = plan->dxor[slot];
     const U* src = static_cast<const U*>(plan->ksrc[slot]);
@@ -804,7 +890,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
 
     // global digit offsets of this slot: exclusive scan of its histogram
     if (tid < kRadix) {
-        const unsigned long long c = plan->hist[slot][tid];
         unsigned long long incl = c;
         const int lane = tid & 31;
 #pragma unroll
@@ -863,18 +948,18 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
                 parity ^= 1u << cur;
                 B2S_PHASE(0);
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, RANK>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t);
+                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, RANK>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t);
+                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, RANK>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR>(
                 claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
-                nd, s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t);
+                nd, s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
         }
         __syncthreads();
         B2S_PHASE(5);
@@ -1434,6 +1519,19 @@ int onesweep_cfg() {
     return cfg;
 }
 
+// A pass is skewed when one digit holds more than n >> B2S_SKEW_SHIFT keys
+// (default 3: an eighth; 64 never). Measured per 2^27-key pass: uniform keys
+// 0.42 ms regular / 0.52 ms hot-digit path; Zipf(1.2) keys, top digit ~20%:
+// 0.557 / 0.525; top digit ~75%: 1.00-1.14 / 0.39-0.48.
+uint64_t skew_limit(uint64_t n) {
+    static int sh = -1;
+    if (sh < 0) {
+        const char* e = getenv("B2S_SKEW_SHIFT");
+        sh = e ? atoi(e) : 3;
+    }
+    return sh >= 64 ? ~0ull : (n >> sh);
+}
+
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
 b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
                                void* lb) {
@@ -1441,12 +1539,26 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
     constexpr int TILE = SM::TILE;
     constexpr size_t SMEM = SM::bytes;
     auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>;
-    static int occ = -1;  // per instantiation, per process (single device type)
+    // the skewed-pass twin (same tile, so the same look-back layout)
+    constexpr int TT = THREADS;
+    constexpr int TI = ITEMS;
+    using SM2 = OnesweepSmem<U, VALS, TT, TI>;
+    static_assert(SM2::TILE == TILE, "the twin shares the look-back layout");
+    constexpr size_t SMEM2 = SM2::bytes;
+    auto skew_kern = onesweep_kernel<U, VALS, LB, TT, TI, MINB, 3>;
+    static int occ = -1, occ2 = -1;  // per instantiation, per process (single device type)
     if (occ < 0) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SMEM));
         int o = 0;
         B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
+        if constexpr (RANK == 2) {
+            B2S_CUDA(cudaFuncSetAttribute(skew_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SMEM2));
+            int o2 = 0;
+            B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, skew_kern, TT, SMEM2));
+            occ2 = o2 > 0 ? o2 : 1;
+        }
         occ = o > 0 ? o : 1;
         if (getenv("B2S_DEBUG")) {
             cudaFuncAttributes fa;
@@ -1460,11 +1572,26 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
     const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ * ctx->num_sms);
     LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
     const int slots = (int)sizeof(U);
+    const uint64_t skew = skew_limit(n);
     for (int s = 0; s < slots; ++s) {
         ctx->ev_pass[s] = record(ctx);
         kern<<<grid, THREADS, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
-                                                      region[(s + 1) & 1]);
+                                                      region[(s + 1) & 1], skew);
         B2S_LAUNCHED();
+        if constexpr (RANK == 2) {  // the twin runs the pass if it is skewed
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ2 * ctx->num_sms));
+            lc.blockDim = dim3(TT);
+            lc.dynamicSmemBytes = SMEM2;
+            lc.stream = ctx->stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            B2S_CUDA(cudaLaunchKernelEx(&lc, skew_kern, plan, ctr, s, n, ntiles, region[s & 1],
+                                        region[(s + 1) & 1], skew));
+        }
     }
     ctx->ev_pass[slots] = record(ctx);
     return B2S_OK;
@@ -1474,7 +1601,7 @@ template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
 b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
                              void* lb) {
     if (ctx->atomic_rank)
-        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 2>(ctx, plan, ctr, n, lb);
     return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 

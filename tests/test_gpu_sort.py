@@ -50,6 +50,9 @@ def rand_keys(n, dt, rng, kind="uniform"):
         shift = ut(np.dtype(dt).itemsize * 8 - 16)
         x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True).view(ut)
         return (x & ~(ut(0xFF) << shift)).view(dt)
+    if kind == "skewed":  # ~60% zeros: passes whose top digit is hot rank by ballots
+        x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        return np.where(rng.random(n) < 0.6, dt(0), x).astype(dt)
     if kind == "extremes":
         return rng.choice(np.array([info.min, info.max, 0, 1, info.max - 1, info.min + 1],
                                    dtype=dt), n)
@@ -80,7 +83,7 @@ def test_sort_uniform_sizes(ctx, dt, n):
 
 @pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("kind", ["dups", "equal", "sorted", "reverse", "topbyte", "extremes",
-                                  "lowzero", "midconst"])
+                                  "lowzero", "midconst", "skewed"])
 def test_sort_distributions(ctx, dt, kind):
     rng = np.random.default_rng(5)
     for n in (5000, 70_001):
@@ -109,7 +112,7 @@ def test_sort_in_place_and_host_buffers(ctx, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
-@pytest.mark.parametrize("kind", ["dups", "uniform", "equal"])
+@pytest.mark.parametrize("kind", ["dups", "uniform", "equal", "skewed"])
 @pytest.mark.parametrize("n", [123_457, 3072, 5121, 1])
 def test_sort_pairs_stable(ctx, dt, kind, n):
     rng = np.random.default_rng(17)
