@@ -62,6 +62,7 @@ struct RadixPlan {
     int num_active;
     int do_copy;
     int need_fallback;  // first active digit is not digit 0: recount it
+    int structured;     // input nearly sorted either way: swizzled staging
     int digit[kMaxSlots];
     uint32_t dxor[kMaxSlots];  // 0x80 on the top digit of signed keys
     const unsigned long long* hist[kMaxSlots];  // digit histogram per slot
@@ -82,6 +83,7 @@ struct RadixCounters {
     unsigned long long spec0[256];            // prologue's digit-0 histogram
     unsigned long long or_all;                // OR of all keys
     unsigned long long nor_all;               // OR of all complemented keys
+    unsigned long long asc_pairs, desc_pairs;  // sampled adjacent pairs in order / reversed
 };
 
 struct TimingEvents {

@@ -109,6 +109,17 @@ __device__ __forceinline__ uint32_t digit_of(U k, int shift, uint32_t dxor) {
 // ---------------------------------------------------------------------------
 // prologue: varying-bit statistics + digit-0 histogram (one read of the keys)
 
+// order statistic of the adjacent pairs inside one vector (the prologue
+// samples one vector in four): structured input is almost all one direction
+template <typename U, int D>
+__device__ __forceinline__ void order_pairs(const U (&e)[D], uint32_t& asc, uint32_t& desc) {
+#pragma unroll
+    for (int j = 0; j + 1 < D; ++j) {
+        asc += e[j] < e[j + 1];
+        desc += e[j + 1] < e[j];
+    }
+}
+
 template <typename U, int D>
 __device__ __forceinline__ void prologue_keys(const U (&e)[D], unsigned long long& o,
                                               unsigned long long& no, uint32_t hbase) {
@@ -121,14 +132,20 @@ __device__ __forceinline__ void prologue_keys(const U (&e)[D], unsigned long lon
     }
 }
 
+// CTAs per SM of the prologue (its grid is exactly one wave of them; 32
+// registers per thread for u32 keys, 40 for u64)
 template <typename U>
-__global__ void __launch_bounds__(512) radix_prologue_kernel(const U* __restrict__ keys, uint64_t n,
+constexpr int kPrologueMinBlocks = sizeof(U) == 4 ? 4 : 3;
+
+template <typename U>
+__global__ void __launch_bounds__(512, kPrologueMinBlocks<U>) radix_prologue_kernel(const U* __restrict__ keys, uint64_t n,
                                                              RadixCounters* __restrict__ ctr,
                                                              uint4* __restrict__ lb_zero,
                                                              uint64_t lb_zero_vecs) {
     constexpr int VEC = 16 / sizeof(U);
     __shared__ uint32_t s_h[kRadix];
     __shared__ unsigned long long s_or[16], s_nor[16];
+    __shared__ uint2 s_ord[16];
     for (int i = threadIdx.x; i < kRadix; i += blockDim.x) s_h[i] = 0;
     __syncthreads();
     const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(s_h);
@@ -137,6 +154,7 @@ __global__ void __launch_bounds__(512) radix_prologue_kernel(const U* __restrict
     for (uint64_t i = tid; i < lb_zero_vecs; i += stride) lb_zero[i] = make_uint4(0, 0, 0, 0);
 
     unsigned long long o = 0, no = 0;
+    uint32_t asc = 0, desc = 0;
     const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
     uint64_t head = 0;
     if (aligned) {
@@ -150,10 +168,12 @@ __global__ void __launch_bounds__(512) radix_prologue_kernel(const U* __restrict
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 prologue_keys<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q[u]), o, no, hbase);
+            order_pairs<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q[0]), asc, desc);
         }
         for (; v < nvec; v += stride) {
             uint4 q = __ldcs(kv + v);
             prologue_keys<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q), o, no, hbase);
+            order_pairs<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q), asc, desc);
         }
         head = nvec * VEC;
     }
@@ -166,20 +186,28 @@ __global__ void __launch_bounds__(512) radix_prologue_kernel(const U* __restrict
     for (int off = 16; off > 0; off >>= 1) {
         o |= __shfl_xor_sync(0xffffffffu, o, off);
         no |= __shfl_xor_sync(0xffffffffu, no, off);
+        asc += __shfl_xor_sync(0xffffffffu, asc, off);
+        desc += __shfl_xor_sync(0xffffffffu, desc, off);
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
         s_or[warp] = o;
         s_nor[warp] = no;
+        s_ord[warp] = make_uint2(asc, desc);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        unsigned long long a = asc, d = desc;
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
             o |= s_or[w];
             no |= s_nor[w];
+            a += s_ord[w].x;
+            d += s_ord[w].y;
         }
         if (o) atomicOr(&ctr->or_all, o);
         if (no) atomicOr(&ctr->nor_all, no);
+        if (a) atomicAdd(&ctr->asc_pairs, a);
+        if (d) atomicAdd(&ctr->desc_pairs, d);
     }
     for (int i = threadIdx.x; i < kRadix; i += blockDim.x) {
         const uint32_t c = s_h[i];
@@ -207,6 +235,14 @@ __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* _
         ++na;
     }
     plan->num_active = na;
+    // structured input (sorted, reverse, nearly so): adjacent pairs almost all
+    // in one direction. Its passes scatter with strided slots, so they run
+    // the bank-swizzled kernel.
+    {
+        const unsigned long long a = ctr->asc_pairs, d = ctr->desc_pairs;
+        const unsigned long long hi = a > d ? a : d, lo = a > d ? d : a;
+        plan->structured = hi > 8 * lo && hi > n / 16;
+    }
     plan->need_fallback = (na > 0 && plan->digit[0] != 0);
     if (na > 0 && plan->digit[0] == 0) plan->hist[0] = ctr->spec0;
     // Buffer chain: slot s writes `out` when (na-1-s) is even, else `tmp`, so
@@ -392,6 +428,20 @@ __device__ __forceinline__ void sts_key(uint32_t a, unsigned long long v) {
     asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
 
+// Bank swizzle of a staged tile slot: slot r sits at r ^ (its 128-byte row
+// index mod the row's element count). Rows stay whole, so the write-out's
+// consecutive reads stay conflict-free, while the ranking's scatter -- whose
+// slots are strided when the input is structured (sorted input: a warp's 32
+// keys go to 32 digit runs of equal length, all on 2 banks) -- spreads over
+// the banks.
+// It costs two ALU ops per key, so only passes over structured input (see
+// radix_plan_kernel) use it.
+template <int BYTES, bool SWZ>
+__device__ __forceinline__ uint32_t swz(uint32_t r) {
+    constexpr uint32_t EPR = 128 / BYTES;  // elements per 128-byte row
+    return SWZ ? r ^ ((r / EPR) & (EPR - 1)) : r;
+}
+
 struct NextDigit {
     int shift;
     uint32_t dxor;
@@ -420,7 +470,8 @@ struct TileShared {
 // Write-out of a staged tile: runs of equal digits go to consecutive global
 // slots (consecutive threads, consecutive positions); the next slot's digit is
 // counted on the way out.
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool AGG = false>
+template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool AGG = false,
+          bool SWZ = false>
 __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbuf,
                                               const typename TileShared<LB>::OFF* gbase,
                                               uint32_t tile_valid, U* __restrict__ dst,
@@ -428,17 +479,24 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
                                               const NextDigit nd) {
     using OFF = typename TileShared<LB>::OFF;
     const bool full = tile_valid == (uint32_t)(THREADS * ITEMS);
+    constexpr uint32_t EPR = 128 / sizeof(U);
+    static_assert(THREADS % EPR == 0, "whole rows per item step");
+    const uint32_t q = threadIdx.x / EPR;
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t i = j * THREADS + threadIdx.x;
         if (full || i < tile_valid) {
-            const U k = kbuf[i];
+            // swz(i) with the row term folded: j * THREADS is a whole number
+            // of rows, so only the low bits of threadIdx.x are permuted
+            const uint32_t si = SWZ ? j * THREADS + (threadIdx.x ^ (((uint32_t)(j * THREADS / EPR) + q) & (EPR - 1)))
+                                            : i;
+            const U k = kbuf[si];
             const OFF g = gbase[digit_of(k, shift, dxor)] + (OFF)i;
 #ifdef B2S_ABLATE_WRITE
             if (k == (U)0x12345678 && g == 0)
 #endif
             __stcs(dst + g, k);
-            if constexpr (VALS) __stcs(vdst + g, vbuf[i]);
+            if constexpr (VALS) __stcs(vdst + g, vbuf[sizeof(U) == 4 ? si : swz<4, SWZ>(i)]);
 #ifndef B2S_ABLATE_NEXTHIST
             if (nd.on) {
                 const uint32_t dn = digit_of(k, nd.shift, nd.dxor);
@@ -459,7 +517,7 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
-          bool PIPE, int RANK, typename Claim, typename Between>
+          bool PIPE, int RANK, bool SWZ = false, typename Claim, typename Between>
 __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Between& between,
                                               typename TileShared<LB>::OFF* gbase_out, uint32_t tile,
                                               uint32_t tile_valid, uint64_t tile_base,
@@ -645,8 +703,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             for (int b = 0; b < B; ++b) {
                 if (j0 + b < ITEMS) {
                     const uint32_t rr = h[b] ? r[b] : (old[b] >> s16[b]) & 0xFFFFu;
-                    sts_key(keys_a + rr * (uint32_t)sizeof(U), keys[j0 + b]);
-                    if constexpr (VALS) sts_key(vals_a + 4 * rr, vals[j0 + b]);
+                    sts_key(keys_a + swz<sizeof(U), SWZ>(rr) * (uint32_t)sizeof(U), keys[j0 + b]);
+                    if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(rr), vals[j0 + b]);
                 }
             }
         }
@@ -671,8 +729,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             for (int b = 0; b < B; ++b) {
                 if (j0 + b < ITEMS) {
                     const uint32_t r = (old[b] >> s16[b]) & 0xFFFFu;
-                    sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j0 + b]);
-                    if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j0 + b]);
+                    sts_key(keys_a + swz<sizeof(U), SWZ>(r) * (uint32_t)sizeof(U), keys[j0 + b]);
+                    if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(r), vals[j0 + b]);
                 }
             }
         }
@@ -722,8 +780,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #else
         if (valid) {
 #endif
-            sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j]);
-            if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j]);
+            sts_key(keys_a + swz<sizeof(U), SWZ>(r) * (uint32_t)sizeof(U), keys[j]);
+            if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(r), vals[j]);
         }
     }
     B2S_PHASE(3);
@@ -805,8 +863,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // ---- write runs of equal digits; clear this warp's counters
 #pragma unroll
     for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
-    writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2>(kbuf, vbuf, gbase_out, tile_valid, dst, vdst,
-                                                          shift, dxor, nd);
+    writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2, SWZ>(kbuf, vbuf, gbase_out, tile_valid, dst,
+                                                               vdst, shift, dxor, nd);
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
@@ -821,16 +879,21 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     constexpr int TILE = SM::TILE;
     static_assert(THREADS >= kRadix, "one thread per digit is required");
     static_assert(TILE < 65536, "packed 16-bit warp counters");
-    // RANK: 0 ballots, 1 atomics; 2 atomics unless the pass is skewed, 3
-    // hot-digit ranking only if it is. Same-address shared atomics serialise
-    // across the lanes that share a digit, so in a pass with a hot digit (more
-    // than skew_limit keys) that digit is counted and ranked by ballots and
-    // the rest by atomics. 2 and 3 are launched back to back per pass, 3 as a
-    // programmatic dependent of 2: its CTAs take the SMs as 2's drain, and the
-    // one not suited to the pass exits at once. The histogram they decide on
-    // was final before 2 started.
-    constexpr int TR = RANK == 3 ? 2 : (RANK == 2 ? 1 : RANK);
-    if constexpr (RANK == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // RANK: 0 ballots, 1 atomics (one kernel per pass), or one of three
+    // kernels launched back to back per pass, exactly one of which runs it:
+    //   2  atomics, unless the pass is skewed or the input structured;
+    //   3  skewed pass (a digit holds more than skew_limit keys): same-address
+    //      shared atomics serialise across the lanes that share a digit, so
+    //      that digit is counted and ranked by ballots, the rest by atomics;
+    //   4  structured input, pass not skewed: atomics + swizzled staging.
+    // 3 and 4 are programmatic dependents of their predecessor: their CTAs
+    // take the SMs as the predecessor's drain, and the ones not suited to the
+    // pass exit at once. What they decide on (the pass's histogram, the
+    // prologue's order statistic) was final before 2 started.
+    constexpr int TR = RANK == 3 ? 2 : (RANK >= 2 ? 1 : RANK);
+    constexpr bool SWZ = RANK == 4;
+    if constexpr (RANK == 2 || RANK == 3)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     const int na = plan->num_active;
     if (slot >= na) return;
@@ -840,9 +903,11 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     uint32_t hot = 0;  // the pass's most frequent digit (RANK 3)
     if constexpr (RANK >= 2) {
         const bool skewed = __syncthreads_or(tid < kRadix && c > skew_limit) != 0;
-        if (skewed != (RANK == 3)) return;
+        const bool structured = plan->structured != 0;
+        const int mode = skewed ? 3 : (structured ? 4 : 2);
+        if (mode != RANK) return;
+        if constexpr (RANK >= 3) asm volatile("griddepcontrol.wait;" ::: "memory");
         if constexpr (RANK == 3) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
             __shared__ unsigned long long s_hot;
             if (tid == 0) s_hot = 0;
             __syncthreads();
@@ -948,16 +1013,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
                 parity ^= 1u << cur;
                 B2S_PHASE(0);
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR, SWZ>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR, SWZ>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR, SWZ>(
                 claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
                 nd, s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
         }
@@ -1538,58 +1603,49 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
     constexpr size_t SMEM = SM::bytes;
-    auto kern = onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>;
-    // the skewed-pass twin (same tile, so the same look-back layout)
-    constexpr int TT = THREADS;
-    constexpr int TI = ITEMS;
-    using SM2 = OnesweepSmem<U, VALS, TT, TI>;
-    static_assert(SM2::TILE == TILE, "the twin shares the look-back layout");
-    constexpr size_t SMEM2 = SM2::bytes;
-    auto skew_kern = onesweep_kernel<U, VALS, LB, TT, TI, MINB, 3>;
-    static int occ = -1, occ2 = -1;  // per instantiation, per process (single device type)
-    if (occ < 0) {
-        B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SMEM));
-        int o = 0;
-        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
-        if constexpr (RANK == 2) {
-            B2S_CUDA(cudaFuncSetAttribute(skew_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)SMEM2));
-            int o2 = 0;
-            B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, skew_kern, TT, SMEM2));
-            occ2 = o2 > 0 ? o2 : 1;
-        }
-        occ = o > 0 ? o : 1;
-        if (getenv("B2S_DEBUG")) {
-            cudaFuncAttributes fa;
-            cudaFuncGetAttributes(&fa, kern);
-            fprintf(stderr, "[b2s] onesweep<%zuB keys, vals=%d, %d thr, %d items, rank=%d>: dyn smem %zu + static %zu B, regs %d, %d CTA/SM\n",
-                    sizeof(U), (int)VALS, THREADS, ITEMS, RANK, (size_t)SMEM, (size_t)fa.sharedSizeBytes, fa.numRegs, occ);
+    // the regular kernel and, for RANK 2, its skewed-pass and structured-input
+    // twins (same tile and shared memory, so the same look-back layout)
+    using Kern = void (*)(RadixPlan*, RadixCounters*, int, uint64_t, uint32_t, LB*, LB*, uint64_t);
+    constexpr int NK = RANK == 2 ? 3 : 1;
+    const Kern kern[3] = {onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>,
+                          onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 3>,
+                          onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 4>};
+    static int occ[3] = {-1, -1, -1};  // per instantiation, per process (single device type)
+    if (occ[0] < 0) {
+        for (int k = 0; k < NK; ++k) {
+            B2S_CUDA(cudaFuncSetAttribute(kern[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SMEM));
+            int o = 0;
+            B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern[k], THREADS, SMEM));
+            occ[k] = o > 0 ? o : 1;
+            if (getenv("B2S_DEBUG")) {
+                cudaFuncAttributes fa;
+                cudaFuncGetAttributes(&fa, kern[k]);
+                fprintf(stderr, "[b2s] onesweep<%zuB keys, vals=%d, %d thr, %d items, rank=%d>: dyn smem %zu + static %zu B, regs %d, %d CTA/SM\n",
+                        sizeof(U), (int)VALS, THREADS, ITEMS, k == 0 ? RANK : k + 2, (size_t)SMEM,
+                        (size_t)fa.sharedSizeBytes, fa.numRegs, occ[k]);
+            }
         }
     }
     const uint64_t ntiles64 = (n + TILE - 1) / TILE;
     const uint32_t ntiles = (uint32_t)ntiles64;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ * ctx->num_sms);
     LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
     const int slots = (int)sizeof(U);
     const uint64_t skew = skew_limit(n);
     for (int s = 0; s < slots; ++s) {
         ctx->ev_pass[s] = record(ctx);
-        kern<<<grid, THREADS, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
-                                                      region[(s + 1) & 1], skew);
-        B2S_LAUNCHED();
-        if constexpr (RANK == 2) {  // the twin runs the pass if it is skewed
+        for (int k = 0; k < NK; ++k) {
             cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3((uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ2 * ctx->num_sms));
-            lc.blockDim = dim3(TT);
-            lc.dynamicSmemBytes = SMEM2;
+            lc.gridDim = dim3((uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ[k] * ctx->num_sms));
+            lc.blockDim = dim3(THREADS);
+            lc.dynamicSmemBytes = SMEM;
             lc.stream = ctx->stream;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             at[0].val.programmaticStreamSerializationAllowed = 1;
             lc.attrs = at;
-            lc.numAttrs = 1;
-            B2S_CUDA(cudaLaunchKernelEx(&lc, skew_kern, plan, ctr, s, n, ntiles, region[s & 1],
+            lc.numAttrs = k > 0 ? 1 : 0;  // the twins are programmatic dependents
+            B2S_CUDA(cudaLaunchKernelEx(&lc, kern[k], plan, ctr, s, n, ntiles, region[s & 1],
                                         region[(s + 1) & 1], skew));
         }
     }
@@ -1724,7 +1780,8 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     {
         const int threads = 512;
         uint64_t want = (n / (16 / sizeof(U)) + threads - 1) / threads;
-        int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)ctx->num_sms * 4);
+        int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1),
+                                           (uint64_t)ctx->num_sms * kPrologueMinBlocks<U>);
         radix_prologue_kernel<U><<<grid, threads, 0, ctx->stream>>>(
             static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(ctx->lookback.ptr),
             (lb_region + 15) / 16);

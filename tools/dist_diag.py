@@ -14,6 +14,8 @@ kind = sys.argv[1]
 n = 1 << 27
 if kind == "zipf":
     k = zipf_keys(ctx, n)
+elif kind == "equal":
+    k = torch.full((n,), 7, dtype=torch.int32, device="cuda")
 elif kind == "asc":
     k = torch.arange(n, dtype=torch.int32, device="cuda")
 else:
@@ -25,4 +27,4 @@ ctx.sort(k, out=out)
 t = ctx.timing()
 ctx.enable_timing(False)
 print(kind, os.environ.get("B2S_LIB", "default").split("/")[-1], os.environ.get("B2S_SKEW_SHIFT"),
-      round(ms, 4), [round(x, 4) for x in t.pass_ms])
+      round(ms, 4), "hist", round(t.hist_ms, 4), "copy", round(t.copy_ms, 4), [round(x, 4) for x in t.pass_ms])
