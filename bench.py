@@ -191,6 +191,7 @@ def run_single(args):
     import numpy as np
     import torch
 
+    from paper_1105_6040_b200 import _lib
     from paper_1105_6040_b200.device import Context
 
     hbm_peak, peak_kind = _peaks()
@@ -218,11 +219,13 @@ def run_single(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    launches0 = _lib.lib().b2s_kernel_launches()
     e0.record(stream)
     for _ in range(args.steps):
         ctx.sort(keys, out=out)
     e1.record(stream)
     torch.cuda.synchronize()
+    launches = _lib.lib().b2s_kernel_launches() - launches0
     total_ms = e0.elapsed_time(e1)
     ms_step = total_ms / args.steps
 
@@ -283,7 +286,7 @@ def run_single(args):
                 "path": f"b2s_sort_batch(B2S_HOST) over {e2e_steps} pinned host batches "
                         "(upload/sort/download of consecutive batches overlapped)",
                 "single_call_ms": e2e_single_s * 1e3},
-        "gpu_launches": args.steps * (3 + executed),
+        "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,
     }
@@ -299,6 +302,7 @@ def run_multi(args, rank: int, world: int):
     import torch
     import torch.distributed as dist
 
+    from paper_1105_6040_b200 import _lib
     from paper_1105_6040_b200.device import Context
     from paper_1105_6040_b200.sample_sort import SampleSorter
 
@@ -323,11 +327,13 @@ def run_multi(args, rank: int, world: int):
     clocks = Clocks(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.lib().b2s_kernel_launches()
     e0.record()
     for _ in range(args.steps):
         sorter.sort(keys)
     e1.record()
     torch.cuda.synchronize()
+    launches = _lib.lib().b2s_kernel_launches() - launches0
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -392,7 +398,7 @@ def run_multi(args, rank: int, world: int):
             "e2e": {"value": total / float(e2e_s.item()), "unit": UNIT,
                     "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": d2h,
                     "path": "SampleSorter.sort from pinned host shards (per rank)"},
-            "gpu_launches": args.steps * (7 + 3 + 2 * rounds),
+            "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": None,
         }

@@ -86,6 +86,9 @@ b2s_status b2s_get_timing(b2s_ctx* ctx, b2s_timing* out);
 const char* b2s_last_error(void);
 const char* b2s_version(void);
 int b2s_device_count(void);
+/* Kernels this library has launched in this process (all contexts); the
+ * difference across a region counts the region's launches. */
+unsigned long long b2s_kernel_launches(void);
 
 /* ---- local sort ----------------------------------------------------------
  * Replaces the per-rank comparison kernels behind KernelFn

@@ -7,6 +7,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -17,7 +18,11 @@ namespace b2s {
 
 namespace {
 thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};
 }
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 b2s_status set_error(b2s_status st, const char* fmt, ...) {
     char buf[1024];
@@ -137,6 +142,8 @@ extern "C" {
 const char* b2s_last_error(void) { return g_err.c_str(); }
 
 const char* b2s_version(void) { return "b200sort 0.1 (sm_100a onesweep radix + merge path)"; }
+
+unsigned long long b2s_kernel_launches(void) { return b2s::launch_count(); }
 
 int b2s_device_count(void) {
     int n = 0;

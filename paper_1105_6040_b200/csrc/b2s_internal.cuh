@@ -27,7 +27,14 @@ void clear_error();
                                     cudaGetErrorString(e_));                             \
     } while (0)
 
-#define B2S_LAUNCHED() B2S_CUDA(cudaGetLastError())
+// every kernel launch of the library is counted (b2s_kernel_launches)
+void note_launch();
+unsigned long long launch_count();
+#define B2S_LAUNCHED()                      \
+    do {                                    \
+        ::b2s::note_launch();               \
+        B2S_CUDA(cudaGetLastError());       \
+    } while (0)
 
 #define B2S_TRY(expr)                                \
     do {                                             \

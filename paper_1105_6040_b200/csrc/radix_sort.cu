@@ -1647,6 +1647,7 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
             lc.numAttrs = k > 0 ? 1 : 0;  // the twins are programmatic dependents
             B2S_CUDA(cudaLaunchKernelEx(&lc, kern[k], plan, ctr, s, n, ntiles, region[s & 1],
                                         region[(s + 1) & 1], skew));
+            note_launch();
         }
     }
     ctx->ev_pass[slots] = record(ctx);

@@ -13,7 +13,11 @@ scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
 agg, cnt = collections.defaultdict(float), collections.Counter()
 for r in rows:
     name = r[ik].split("(")[0].replace("void ", "").replace("b2s::<unnamed>::", "")
-    name = name.split("<")[0]
+    if "onesweep_kernel<" in name:  # keep the mode (last template argument)
+        mode = name.split("<", 1)[1].rstrip(">").split(",")[-1].strip().replace("(int)", "")
+        name = name.split("<")[0] + f"[mode {mode}]"
+    else:
+        name = name.split("<")[0]
     agg[name] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1e-3)
     cnt[name] += 1
 tot = sum(agg.values())
