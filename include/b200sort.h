@@ -90,6 +90,22 @@ int b2s_device_count(void);
  * difference across a region counts the region's launches. */
 unsigned long long b2s_kernel_launches(void);
 
+/* ---- multi-GPU pull exchange (one process per GPU) ------------------------
+ * Replaces the reference's rank-to-rank block messages (Comm::send/recv and
+ * gather, P/src/runtime.cpp:219-328,547-568): every rank exports the buffer
+ * holding its sorted shard, maps its peers' buffers, and its merge kernel
+ * reads its bucket's slice of every peer's shard straight over NVLink.
+ *
+ * b2s_exchange_buffer: a device buffer of at least `bytes` owned by the
+ *   context (reused across calls, reallocated when it must grow) and its CUDA
+ *   IPC handle (64 bytes) for the peers.
+ * b2s_open_peer: maps a peer's buffer from its handle (cached per handle;
+ *   the same process may not open its own handle).
+ * b2s_close_peers: unmaps every peer buffer this context opened. */
+b2s_status b2s_exchange_buffer(b2s_ctx* ctx, uint64_t bytes, void** ptr, void* handle64);
+b2s_status b2s_open_peer(b2s_ctx* ctx, const void* handle64, void** ptr);
+b2s_status b2s_close_peers(b2s_ctx* ctx);
+
 /* ---- local sort ----------------------------------------------------------
  * Replaces the per-rank comparison kernels behind KernelFn
  * (P/include/sortbench/parallel_sort.hpp:69-72; kernels::merge_sort /

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -145,6 +146,50 @@ const char* b2s_version(void) { return "b200sort 0.1 (sm_100a onesweep radix + m
 
 unsigned long long b2s_kernel_launches(void) { return b2s::launch_count(); }
 
+b2s_status b2s_exchange_buffer(b2s_ctx* ctx, uint64_t bytes, void** ptr, void* handle64) {
+    B2S_TRY(check_ctx(ctx));
+    if (ptr == nullptr || handle64 == nullptr) return set_error(B2S_EINVAL, "null output");
+    // peers may still be reading the current buffer: reallocation waits for
+    // this context's stream (the caller orders the peers' reads before it)
+    if (bytes > ctx->xbuf.bytes) B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    B2S_TRY(ctx->xbuf.ensure(bytes));
+    if (ctx->xbuf_handle_ptr != ctx->xbuf.ptr) {
+        cudaIpcMemHandle_t h;
+        B2S_CUDA(cudaIpcGetMemHandle(&h, ctx->xbuf.ptr));
+        memcpy(ctx->xbuf_handle, &h, sizeof h);
+        ctx->xbuf_handle_ptr = ctx->xbuf.ptr;
+    }
+    *ptr = ctx->xbuf.ptr;
+    memcpy(handle64, ctx->xbuf_handle, 64);
+    return B2S_OK;
+}
+
+b2s_status b2s_open_peer(b2s_ctx* ctx, const void* handle64, void** ptr) {
+    B2S_TRY(check_ctx(ctx));
+    if (ptr == nullptr || handle64 == nullptr) return set_error(B2S_EINVAL, "null argument");
+    const std::string key(static_cast<const char*>(handle64), 64);
+    auto it = ctx->peers.find(key);
+    if (it != ctx->peers.end()) {
+        *ptr = it->second;
+        return B2S_OK;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof h);
+    void* p = nullptr;
+    B2S_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->peers.emplace(key, p);
+    *ptr = p;
+    return B2S_OK;
+}
+
+b2s_status b2s_close_peers(b2s_ctx* ctx) {
+    B2S_TRY(check_ctx(ctx));
+    B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& kv : ctx->peers) B2S_CUDA(cudaIpcCloseMemHandle(kv.second));
+    ctx->peers.clear();
+    return B2S_OK;
+}
+
 int b2s_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -201,10 +246,12 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
     if (ctx == nullptr) return B2S_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->peers) cudaIpcCloseMemHandle(kv.second);
+    ctx->peers.clear();
     DevBuf* bufs[] = {&ctx->alt_keys, &ctx->alt_vals,  &ctx->seg_keys,  &ctx->seg_vals,
                       &ctx->lookback, &ctx->hist,      &ctx->plan,      &ctx->parts,
                       &ctx->misc,     &ctx->stage_in,  &ctx->stage_out, &ctx->stage_vin,
-                      &ctx->stage_vout};
+                      &ctx->stage_vout, &ctx->xbuf};
     for (DevBuf* b : bufs) b->release();
     ctx->host_misc.release();
     for (int i = 0; i < 40; ++i)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -117,6 +118,12 @@ struct b2s_ctx {
     b2s::HostBuf host_misc;              // pinned small results
     // B2S_HOST staging
     b2s::DevBuf stage_in, stage_out, stage_vin, stage_vout;
+    // multi-GPU pull exchange: this rank's IPC-exported buffer (its sorted
+    // shard) and the peers' buffers mapped into this process
+    b2s::DevBuf xbuf;
+    void* xbuf_handle_ptr = nullptr;  // allocation the cached handle belongs to
+    unsigned char xbuf_handle[64] = {};
+    std::map<std::string, void*> peers;  // IPC handle bytes -> mapped pointer
 
     bool timing = false;
     cudaEvent_t ev[40] = {};

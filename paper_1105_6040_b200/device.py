@@ -226,6 +226,48 @@ class Context:
             ctypes.byref(nv), B2S_HOST if host else B2S_DEVICE))
         return out[: nr.value], nv.value
 
+    # -- multi-GPU pull exchange ------------------------------------------------
+    def exchange_buffer(self, nbytes: int):
+        """(device pointer, 64-byte IPC handle) of this context's exported
+        buffer, grown to at least `nbytes`."""
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        check(lib().b2s_exchange_buffer(self._h, nbytes, ctypes.byref(p), h))
+        return p.value, h.raw
+
+    def open_peer(self, handle: bytes) -> int:
+        """Device pointer of a peer's exported buffer (mapped once per handle)."""
+        if len(handle) != 64:
+            raise ValueError("an IPC handle is 64 bytes")
+        p = ctypes.c_void_p()
+        check(lib().b2s_open_peer(self._h, ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
+        return p.value
+
+    def close_peers(self) -> None:
+        check(lib().b2s_close_peers(self._h))
+
+    def view(self, ptr: int, n: int, dtype):
+        """A torch tensor over n elements of device memory at `ptr` (no copy;
+        the memory belongs to this context)."""
+        wire = {torch.uint32: torch.int32, torch.uint64: torch.int64}.get(dtype, dtype)
+        code = {torch.int32: "<i4", torch.int64: "<i8"}[wire]
+        holder = _CudaArray(ptr, n, code)
+        t = torch.as_tensor(holder, device=f"cuda:{self.device}")
+        return t.view(dtype) if wire is not dtype else t
+
+    def merge_ptrs(self, dtype, ptrs, lens, out, vptrs=None, vals_out=None, stream=None):
+        """k-way merge of device runs given as raw pointers (peer memory
+        included) into the device tensor `out`."""
+        k = len(ptrs)
+        rp = (ctypes.c_void_p * k)(*[p if n else None for p, n in zip(ptrs, lens)])
+        ln = (ctypes.c_uint64 * k)(*lens)
+        vp = ((ctypes.c_void_p * k)(*[p if n else None for p, n in zip(vptrs, lens)])
+              if vptrs is not None else None)
+        self._bind_stream(stream)
+        check(lib().b2s_merge(self._h, _torch_dtypes()[dtype], rp, vp, ln, k, _ptr(out),
+                              _ptr(vals_out), B2S_DEVICE))
+        return out, vals_out
+
     # -- sample sort steps (device tensors) -----------------------------------
     def sample_regular(self, sorted_keys, rank: int, samples: int, out=None, stream=None):
         """(samples, 2) uint64 tensor of (order key, rank<<40 | position) records."""
@@ -302,6 +344,14 @@ class Context:
                     ok = v.dtype in (torch.int32, torch.uint32)
                 if not ok:
                     raise TypeError("the payload is 32-bit (uint32 / int32)")
+
+
+class _CudaArray:
+    """__cuda_array_interface__ of a raw device range, for torch.as_tensor."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
 
 
 def _numel(x) -> int:

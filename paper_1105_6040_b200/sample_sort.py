@@ -16,6 +16,15 @@ with exactly ONE data exchange:
   6. counts exchange, then the variable all-to-all of keys     (NCCL all_to_all)
   7. stable k-way merge of the G received runs                 (b2s_merge)
 
+transport="p2p" fuses 6 and 7: the local sort writes into the context's
+IPC-exported buffer (b2s_exchange_buffer), the ranks all-gather their bucket
+bounds and buffer handles (a few hundred bytes), and each rank's merge kernel
+reads its slice of every peer's sorted shard straight over NVLink
+(b2s_open_peer + b2s_merge on peer pointers): no receive buffer, no separate
+all-to-all, the exchange overlaps the merge tile by tile. A stream-ordered
+all-reduce after the merge keeps every rank from re-sorting into its buffer
+while peers still read it.
+
 Bucket r (the output on rank r) is the r-th slice of the global order, so the
 ranks' outputs concatenated in rank order are the sorted input -- the array the
 reference gathers at its master. Because records compare as (key, rank,
@@ -60,6 +69,9 @@ class CudaOps:
     def merge(self, runs, vals):
         return self.ctx.merge(runs, vals=vals)
 
+    def sort_into(self, keys, vals, out, vals_out):
+        return self.ctx.sort(keys, out=out, vals=vals, vals_out=vals_out)
+
     def check(self, keys):
         return self.ctx.check_sorted(keys)
 
@@ -69,7 +81,13 @@ class SampleSorter:
     process group; returns this rank's bucket of the global order."""
 
     def __init__(self, ctx=None, group=None, samples_per_rank: int = 64, ops=None,
-                 force_exchange: bool = False):
+                 force_exchange: bool = False, transport: str = "nccl"):
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"unknown transport {transport!r} (nccl or p2p)")
+        if transport == "p2p" and ctx is None:
+            raise ValueError("the p2p transport needs a device context")
+        self.ctx = ctx
+        self.transport = transport
         self.group = group
         self.force_exchange = force_exchange
         self.samples = samples_per_rank
@@ -87,6 +105,8 @@ class SampleSorter:
         return dist.get_world_size(self.group)
 
     def sort(self, keys: torch.Tensor, vals: torch.Tensor | None = None):
+        if self.transport == "p2p":
+            return self._sort_p2p(keys, vals)
         rank, world = self.rank, self.world
         ev = _Events(self._timing)
         ev.mark("start")
@@ -128,6 +148,74 @@ class SampleSorter:
             out_k, out_v = self.ops.merge(runs, vruns)
         ev.mark("merge")
         self.last_bucket_sizes = recv
+        ev.finish(self)
+        return out_k, out_v
+
+    def _sort_p2p(self, keys: torch.Tensor, vals: torch.Tensor | None):
+        rank, world = self.rank, self.world
+        ctx = self.ctx
+        gloo = dist.get_backend(self.group) == "gloo"  # functional tests: host collectives
+        ev = _Events(self._timing)
+        ev.mark("start")
+        n, kb = keys.numel(), keys.element_size()
+        voff = (n * kb + 255) // 256 * 256
+        base, handle = ctx.exchange_buffer(max(voff + (4 * n if vals is not None else 0), 256))
+        skeys = ctx.view(base, n, keys.dtype)
+        svals = ctx.view(base + voff, n, vals.dtype) if vals is not None else None
+        self.ops.sort_into(keys, vals, skeys, svals)
+        ev.mark("local_sort")
+
+        samples = self.ops.sample(skeys, rank, self.samples)
+        gathered = torch.empty((world * self.samples, 2), dtype=samples.dtype,
+                               device=samples.device)
+        if gloo:
+            g = gathered.cpu()
+            dist.all_gather_into_tensor(_wire(g), _wire(samples.cpu()), group=self.group)
+            gathered.copy_(g)
+        else:
+            dist.all_gather_into_tensor(_wire(gathered), _wire(samples.contiguous()),
+                                        group=self.group)
+        splitters = self.ops.select(gathered, world)
+        bounds = self.ops.bounds(skeys, rank, splitters, world)
+        ev.mark("splitters")
+
+        # every rank's bounds, buffer handle and payload offset: world x (G+1+8+1)
+        hdl = torch.frombuffer(bytearray(handle), dtype=torch.int64)
+        info = torch.cat([bounds.to(torch.int64).cpu(), hdl, torch.tensor([voff])])
+        if gloo:
+            allinfo = torch.empty(world * info.numel(), dtype=torch.int64)
+            dist.all_gather_into_tensor(allinfo, info, group=self.group)
+        else:
+            allinfo = torch.empty(world * info.numel(), dtype=torch.int64, device=keys.device)
+            dist.all_gather_into_tensor(allinfo, info.to(keys.device), group=self.group)
+            allinfo = allinfo.cpu()
+        allinfo = allinfo.view(world, -1)
+        rows = allinfo.tolist()
+        ptrs, vptrs, lens = [], [], []
+        for r, row in enumerate(rows):
+            lo, hi = row[rank], row[rank + 1]
+            h = allinfo[r, world + 1:world + 9].numpy().tobytes()
+            peer = base if r == rank else ctx.open_peer(h)
+            ptrs.append(peer + lo * kb)
+            vptrs.append(peer + row[world + 9] + lo * 4)
+            lens.append(hi - lo)
+        total = sum(lens)
+        ev.mark("exchange")
+
+        out_k = torch.empty(total, dtype=keys.dtype, device=keys.device)
+        out_v = torch.empty(total, dtype=vals.dtype, device=keys.device) if vals is not None else None
+        if total:
+            ctx.merge_ptrs(keys.dtype, ptrs, lens, out_k,
+                           vptrs if vals is not None else None, out_v)
+        ev.mark("merge")
+        # release: nobody re-sorts into its buffer before every peer has read it
+        if gloo:
+            torch.cuda.synchronize(keys.device)
+            dist.barrier(group=self.group)
+        else:
+            flag = torch.zeros(1, dtype=torch.int32, device=keys.device)
+            dist.all_reduce(flag, group=self.group)
+        self.last_bucket_sizes = lens
         ev.finish(self)
         return out_k, out_v
 

@@ -87,19 +87,23 @@ def test_emulated_ranks(ctx, world, kind, dt, with_vals):
     assert max(len(o) for o in outs) <= 2 * n / world + 64 * world
 
 
-def test_distributed_path_nccl_world1(ctx):
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_distributed_path_nccl_world1(ctx, transport):
     import torch.distributed as dist
 
     from paper_1105_6040_b200.sample_sort import SampleSorter
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
     try:
         keys = ctx.gen_keys(1 << 20, 3, torch.int32, shift=33)
         vals = torch.arange(1 << 20, dtype=torch.int32, device="cuda")
-        sorter = SampleSorter(ctx, force_exchange=True)
+        sorter = SampleSorter(ctx, force_exchange=True, transport=transport)
         k, v = sorter.sort(keys, vals)
         assert sorter.verify(k, keys)
         ek, ev = oracle.stable_sort_kv(keys.cpu().numpy(), np.arange(1 << 20, dtype=np.uint32))
@@ -108,3 +112,79 @@ def test_distributed_path_nccl_world1(ctx):
         assert set(sorter.last_phase_ms) >= {"local_sort", "splitters", "exchange", "merge"}
     finally:
         dist.destroy_process_group()
+
+
+def _p2p_rank(rank, world, port, kind, dt, with_vals, n, q):
+    """One rank of the pull-exchange test: its own process and context on the
+    one GPU; peers' sorted shards are mapped through CUDA IPC and read by this
+    rank's merge kernel. Host collectives (gloo) order the steps: no kernel
+    waits on another rank."""
+    import torch.distributed as dist
+
+    from paper_1105_6040_b200.device import Context
+    from paper_1105_6040_b200.sample_sort import SampleSorter
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ctx = Context(0)
+        full = make_input(kind, n, dt)
+        sizes = oracle.plan_partition(n, world)
+        off = sum(sizes[:rank])
+        keys = dev(full[off: off + sizes[rank]])
+        vals = dev(np.arange(off, off + sizes[rank], dtype=np.uint32)) if with_vals else None
+        sorter = SampleSorter(ctx, transport="p2p")
+        outs = []
+        for _ in range(2):  # the second sort reuses the mapped buffers
+            k, v = sorter.sort(keys, vals)
+            outs.append((host(k), host(v) if v is not None else None))
+        res = [None] * world
+        dist.all_gather_object(res, outs)
+        if rank == 0:
+            q.put(res)
+        dist.barrier()
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind,dt,with_vals", [("uniform", np.int32, True),
+                                               ("equal", np.uint64, True),
+                                               ("zipf", np.int32, False)])
+def test_p2p_pull_exchange_processes(world, kind, dt, with_vals):
+    """The p2p transport across `world` processes on the one GPU (CUDA IPC
+    works between processes on the same device): each rank's bucket is pulled
+    from every peer's exported shard by its merge kernel."""
+    import torch.multiprocessing as mp
+    n = 300_007
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    procs = [mpc.Process(target=_p2p_rank, args=(r, world, port, kind, dt, with_vals, n, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    import queue
+    import time
+    res, t0 = None, time.time()
+    while res is None:
+        try:
+            res = q.get(timeout=2)
+        except queue.Empty:
+            bad = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if bad or time.time() - t0 > 300:
+                for p in procs:
+                    p.kill()
+                pytest.fail(f"rank processes failed: exit codes {[p.exitcode for p in procs]}")
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    full = make_input(kind, n, dt)
+    for it in range(2):
+        got = np.concatenate([res[r][it][0] for r in range(world)])
+        if with_vals:
+            ek, ev = oracle.stable_sort_kv(full, np.arange(n, dtype=np.uint32))
+            assert np.array_equal(got, ek)
+            assert np.array_equal(np.concatenate([res[r][it][1] for r in range(world)]).view(np.uint32), ev)
+        else:
+            assert np.array_equal(got, oracle.sort(full))
