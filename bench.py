@@ -316,7 +316,14 @@ def run_multi(args, rank: int, world: int):
     total = n_local * world
     # shard r holds keys [r*n_local, (r+1)*n_local) of the cfg3 stream (int32 = z >> 33)
     keys = ctx.gen_keys(n_local, 1, torch.int32, shift=33, first=rank * n_local)
-    sorter = SampleSorter(ctx, samples_per_rank=64, force_exchange=args.force_dist)
+    transport, transport_note = args.transport, None
+    if transport == "p2p":
+        probe = SampleSorter(ctx, transport="p2p")
+        ok, err = probe.p2p_available()
+        if not ok:  # every rank takes the same branch (collective probe)
+            transport, transport_note = "nccl", f"p2p unavailable on this box: {err or 'a peer failed'}"
+    sorter = SampleSorter(ctx, samples_per_rank=64, force_exchange=args.force_dist,
+                          transport=transport)
     out, _ = sorter.sort(keys)
     if not sorter.verify(out, keys):
         raise RuntimeError(f"rank {rank}: sample sort verification failed")
@@ -387,6 +394,10 @@ def run_multi(args, rank: int, world: int):
             "data": "synthetic (gen_data splitmix64 seed 1 >> 33, int32 in [0, 2^31))",
             "config": {"workload": WORKLOAD_N,
                        "n_per_gpu": n_local, "parallelism": f"sample sort over {world} GPUs",
+                       "exchange": ("merge kernels pull buckets from peer shards over NVLink "
+                                    "(CUDA IPC)" if transport == "p2p" else
+                                    "NCCL all_to_all + k-way merge"),
+                       "exchange_note": transport_note,
                        "l2": "inputs larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": _traffic(n_local),
@@ -418,6 +429,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--ref-sample", type=int, default=1 << 24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU exchange: merge kernels pull from peers over NVLink "
+                         "(CUDA IPC), or NCCL all-to-all + merge")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU sample-sort path even at world size 1")
     args = ap.parse_args()

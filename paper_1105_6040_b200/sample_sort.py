@@ -151,6 +151,33 @@ class SampleSorter:
         ev.finish(self)
         return out_k, out_v
 
+    def p2p_available(self) -> tuple[bool, str]:
+        """Collective probe of the p2p transport: every rank exports its buffer
+        and maps every peer's. All ranks get the same answer (False when any
+        rank failed), plus this rank's error text."""
+        world, dev = self.world, torch.device("cuda", self.ctx.device)
+        gloo = dist.get_backend(self.group) == "gloo"
+        err = ""
+        try:
+            _, handle = self.ctx.exchange_buffer(256)
+        except Exception as e:  # noqa: BLE001 - reported, decided collectively
+            handle, err = bytes(64), str(e)
+        mine = torch.frombuffer(bytearray(handle), dtype=torch.int64)
+        allh = torch.empty(world * 8, dtype=torch.int64, device="cpu" if gloo else dev)
+        dist.all_gather_into_tensor(allh, mine if gloo else mine.to(dev), group=self.group)
+        allh = allh.cpu().view(world, 8)
+        if not err:
+            for r in range(world):
+                if r != self.rank:
+                    try:
+                        self.ctx.open_peer(allh[r].numpy().tobytes())
+                    except Exception as e:  # noqa: BLE001
+                        err = str(e)
+                        break
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device="cpu" if gloo else dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(ok.item()), err
+
     def _sort_p2p(self, keys: torch.Tensor, vals: torch.Tensor | None):
         rank, world = self.rank, self.world
         ctx = self.ctx
