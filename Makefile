@@ -42,12 +42,13 @@ $(LIB)/libb200sort_prof.so: $(SRC)/*.cu $(HDRS)
 lbexp:
 	for w in 0; do mkdir -p build/lb$$w; for f in $(CU); do $(NVCC) $(NVFLAGS) -DB2S_MATCH_HYBRID=$$w -c $(SRC)/$$f.cu -o build/lb$$w/$$f.o || exit 1; done; $(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_lb$$w.so $(addprefix build/lb$$w/,$(addsuffix .o,$(CU))) -lcudart; done
 
-# one experimental build of radix_sort.cu: make variant NAME=x DEFS="-DFOO=1"
+# one experimental build of one source: make variant NAME=x DEFS="-DFOO=1" [VSRC=merge_path]
 # -> lib/libb200sort_x.so (select with B2S_LIB)
+VSRC ?= radix_sort
 variant: $(OBJS)
 	@mkdir -p build/v_$(NAME)
-	$(NVCC) $(NVFLAGS) $(DEFS) -Xptxas -v -c $(SRC)/radix_sort.cu -o build/v_$(NAME)/radix_sort.o 2> build/v_$(NAME)/ptxas.txt || (cat build/v_$(NAME)/ptxas.txt; exit 1)
-	$(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_$(NAME).so build/v_$(NAME)/radix_sort.o $(filter-out $(OBJ)/radix_sort.o,$(OBJS)) -lcudart
+	$(NVCC) $(NVFLAGS) $(DEFS) -Xptxas -v -c $(SRC)/$(VSRC).cu -o build/v_$(NAME)/$(VSRC).o 2> build/v_$(NAME)/ptxas.txt || (cat build/v_$(NAME)/ptxas.txt; exit 1)
+	$(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_$(NAME).so build/v_$(NAME)/$(VSRC).o $(filter-out $(OBJ)/$(VSRC).o,$(OBJS)) -lcudart
 
 oracle:
 	bash oracle/build_ref.sh

@@ -55,14 +55,33 @@ __device__ __forceinline__ uint32_t merge_path_smem(const T* a, uint32_t na, con
     return lo;
 }
 
+// one element global -> shared, asynchronously (LDGSTS)
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if constexpr (sizeof(T) == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
 constexpr int kMergeThreads = 256;
 template <typename T>
 struct MergeItems {
-    static constexpr int value = sizeof(T) == 4 ? 15 : 11;  // odd: conflict-free restaging
+#ifdef B2S_MERGE_ITEMS
+    static constexpr int value = sizeof(T) == 4 ? B2S_MERGE_ITEMS : B2S_MERGE_ITEMS64;
+#else
+    // odd: conflict-free restaging. u32 2-way round of 2^28 keys: 11 items
+    // 0.607 ms, 15: 0.572, 19: 0.555, 23: 0.558; u64 round of 2^27: 7 items
+    // 0.562 ms, 11: 0.485, 15: 0.459 (19 overflows 48 KB with a payload)
+    static constexpr int value = sizeof(T) == 4 ? 19 : 15;
+#endif
 };
 
 // Merges output positions [out_lo, out_hi) of merge(A, B) into out[0 ..).
 // Used both for full merges (out_lo = 0) and for merge_split's kept half.
+// (A persistent variant that streams tile t + gridDim.x into a second buffer
+// while tile t merges measured slower: 2.21 vs 1.78 ms for 8 runs of 2^25.)
 template <typename T, bool VALS>
 __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     const T* __restrict__ a, const uint32_t* __restrict__ va, uint64_t na,
@@ -71,39 +90,42 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     uint32_t* __restrict__ vout) {
     constexpr int ITEMS = MergeItems<T>::value;
     constexpr int TILE = kMergeThreads * ITEMS;
-    __shared__ T s_k[TILE];
+    __shared__ T s_k[TILE + 1];  // +1: the merge loop may read one past the end
     __shared__ uint32_t s_v[VALS ? TILE : 1];
 
     const uint64_t t = blockIdx.x;
     const uint64_t d0 = out_lo + t * TILE;
     const uint64_t d1 = std::min<uint64_t>(d0 + TILE, out_hi);
     const uint64_t a0 = parts[t], a1 = parts[t + 1];
-    const uint64_t b0 = d0 - a0, b1 = d1 - a1;
-    const uint32_t la = (uint32_t)(a1 - a0), lb = (uint32_t)(b1 - b0);
-    const uint32_t cnt = la + lb;
+    const uint64_t b0 = d0 - a0;
+    const uint32_t la = (uint32_t)(a1 - a0), cnt = (uint32_t)(d1 - d0), lb = cnt - la;
 
-    for (uint32_t i = threadIdx.x; i < la; i += kMergeThreads) {
-        s_k[i] = a[a0 + i];
-        if constexpr (VALS) s_v[i] = va[a0 + i];
+    // stage A's slice then B's with asynchronous copies (no registers held,
+    // every copy of the tile in flight at once)
+    for (uint32_t i = threadIdx.x; i < cnt; i += kMergeThreads) {
+        cp_async_elem(&s_k[i], i < la ? a + a0 + i : b + b0 + (i - la));
+        if constexpr (VALS) cp_async_elem(&s_v[i], i < la ? va + a0 + i : vb + b0 + (i - la));
     }
-    for (uint32_t i = threadIdx.x; i < lb; i += kMergeThreads) {
-        s_k[la + i] = b[b0 + i];
-        if constexpr (VALS) s_v[la + i] = vb[b0 + i];
-    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     const uint32_t diag = std::min<uint32_t>(threadIdx.x * ITEMS, cnt);
     uint32_t ai = merge_path_smem(s_k, la, s_k + la, lb, diag);
-    uint32_t bi = diag - ai;
+    uint32_t bi = la + diag - ai;  // index into the staged B
+    // the two heads live in registers: one shared load per output
+    T ka = s_k[ai], kb = s_k[bi];
     T rk[ITEMS];
     uint32_t rv[VALS ? ITEMS : 1];
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         if (diag + j < cnt) {
-            const bool take_a = bi >= lb || (ai < la && !(s_k[la + bi] < s_k[ai]));
-            const uint32_t src = take_a ? ai++ : la + bi++;
-            rk[j] = s_k[src];
-            if constexpr (VALS) rv[j] = s_v[src];
+            const bool take_a = bi >= cnt || (ai < la && !(kb < ka));
+            rk[j] = take_a ? ka : kb;
+            if constexpr (VALS) rv[j] = s_v[take_a ? ai : bi];
+            const uint32_t nxt = take_a ? ++ai : ++bi;
+            const T kn = s_k[nxt];
+            if (take_a) ka = kn;
+            else kb = kn;
         }
     }
     __syncthreads();
@@ -116,9 +138,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     }
     __syncthreads();
     const uint64_t o = d0 - out_lo;
-    for (uint32_t i = threadIdx.x; i < cnt; i += kMergeThreads) {
-        out[o + i] = s_k[i];
-        if constexpr (VALS) vout[o + i] = s_v[i];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t i = threadIdx.x + j * kMergeThreads;
+        if (i < cnt) {
+            __stcs(out + o + i, s_k[i]);
+            if constexpr (VALS) __stcs(vout + o + i, s_v[i]);
+        }
     }
 }
 

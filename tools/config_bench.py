@@ -93,13 +93,16 @@ def main():
     # cfg3 per-GPU work at G=8: local sort of a 2^28 shard + merge of 8 runs
     shard = ctx.gen_keys(1 << 28, 1, torch.int32, shift=33)
     sort_case("cfg3", "per-GPU local sort (2^28 i32 shard)", shard)
-    srt, _ = ctx.sort(shard)
-    runs = [ctx.sort(r.contiguous())[0] for r in torch.tensor_split(srt, 8)]
-    mout = torch.empty_like(srt)
+    # the 8 runs a GPU receives cover the same key range (each is one source's
+    # slice of this bucket): sorted eighths of the random shard, interleaved
+    runs = [ctx.sort(r.contiguous())[0] for r in torch.tensor_split(shard, 8)]
+    mout = torch.empty_like(shard)
     ms = timed(lambda: ctx.merge(runs, out=mout))
-    record("cfg3", "per-GPU merge of 8 received runs (2^28 i32)", 1 << 28, ms,
+    inv, _, _ = ctx.check_sorted(mout)
+    assert inv == 0
+    record("cfg3", "per-GPU merge of 8 received runs (2^28 i32, interleaved)", 1 << 28, ms,
            {"merge_gbs_per_round": round(3 * 8 * (1 << 28) / (ms * 1e-3) / 1e9)})
-    del shard, srt, runs, mout
+    del shard, runs, mout
     torch.cuda.empty_cache()
 
     n4 = 1 << 27
