@@ -25,6 +25,8 @@ std::atomic<unsigned long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+
+
 b2s_status set_error(b2s_status st, const char* fmt, ...) {
     char buf[1024];
     va_list ap;
@@ -251,7 +253,11 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->alt_keys, &ctx->alt_vals,  &ctx->seg_keys,  &ctx->seg_vals,
                       &ctx->lookback, &ctx->hist,      &ctx->plan,      &ctx->parts,
                       &ctx->misc,     &ctx->stage_in,  &ctx->stage_out, &ctx->stage_vin,
-                      &ctx->stage_vout, &ctx->xbuf};
+                      &ctx->stage_vout, &ctx->xbuf, &ctx->seg_lookback, &ctx->seg_hist,
+                      &ctx->seg_plan};
+    for (cudaStream_t s : ctx->side) cudaStreamDestroy(s);
+    for (cudaEvent_t e : ctx->side_done) cudaEventDestroy(e);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
     for (DevBuf* b : bufs) b->release();
     ctx->host_misc.release();
     for (int i = 0; i < 40; ++i)
@@ -520,32 +526,8 @@ b2s_status b2s_partitioned_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, v
         }
         return B2S_OK;
     }
-    // scatter (plan_partition) + local sort of each partition into seg_*
-    std::vector<uint64_t> sizes(p);
-    b2s_plan_partition(n, p, sizes.data());
-    B2S_TRY(ctx->seg_keys.ensure(n * ksz));
-    if (dvin) B2S_TRY(ctx->seg_vals.ensure(n * 4));
-    std::vector<const void*> runs;
-    std::vector<const uint32_t*> vruns;
-    std::vector<uint64_t> lens;
-    uint64_t off = 0;
-    for (int r = 0; r < p; ++r) {
-        const char* src = static_cast<const char*>(din) + off * ksz;
-        char* dst = static_cast<char*>(ctx->seg_keys.ptr) + off * ksz;
-        const uint32_t* vs = dvin ? dvin + off : nullptr;
-        uint32_t* vd = dvin ? static_cast<uint32_t*>(ctx->seg_vals.ptr) + off : nullptr;
-        if (sizes[r]) B2S_TRY(radix_sort(ctx, dtype, src, dst, vs, vd, sizes[r]));
-        runs.push_back(dst);
-        vruns.push_back(vd);
-        lens.push_back(sizes[r]);
-        off += sizes[r];
-    }
-    ctx->have_sort = p == 1;
-    // root merge of the p sorted runs
-    B2S_TRY(ctx->alt_keys.ensure(n * ksz));
-    if (dvin) B2S_TRY(ctx->alt_vals.ensure(n * 4));
-    B2S_TRY(kway_merge(ctx, dtype, runs.data(), dvin ? vruns.data() : nullptr, lens.data(), p,
-                       dout, dvout, ctx->alt_keys.ptr, static_cast<uint32_t*>(ctx->alt_vals.ptr)));
+    B2S_TRY(partitioned_sort_dev(ctx, dtype, din, dout, dvin, dvout, n, p));
+    ctx->have_sort = false;
     ctx->have_merge = true;
     if (flags & B2S_HOST) {
         B2S_TRY(d2h_sync(ctx, out, dout, n * ksz));
@@ -553,6 +535,85 @@ b2s_status b2s_partitioned_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, v
     }
     return B2S_OK;
 }
+
+extern "C++" {
+namespace b2s {
+// scatter (plan_partition) + local sort of each partition + root merge, all
+// asynchronous on ctx->stream
+b2s_status partitioned_sort_dev(b2s_ctx* ctx, b2s_dtype dtype, const void* din, void* dout,
+                                const uint32_t* dvin, uint32_t* dvout, uint64_t n, int p) {
+    const size_t ksz = (size_t)key_bytes(dtype);
+    std::vector<uint64_t> sizes(p);
+    b2s_plan_partition(n, p, sizes.data());
+    B2S_TRY(ctx->seg_keys.ensure(n * ksz));
+    if (dvin) B2S_TRY(ctx->seg_vals.ensure(n * 4));
+    B2S_TRY(ctx->alt_keys.ensure(n * ksz));
+    if (dvin) B2S_TRY(ctx->alt_vals.ensure(n * 4));
+    // The p local sorts run concurrently, each on a side stream with its own
+    // scratch (alt slice, look-back, counters, plan): a partition sort of a
+    // few million keys fills a fraction of the SMs and is bound by its chain
+    // of dependent launches. With timing on they run in order on the stream.
+    const bool conc = !ctx->timing && p > 1;
+    const int nside = std::min(p, kSideStreams);
+    std::vector<size_t> lb_off(p + 1, 0);
+    for (int r = 0; r < p; ++r) lb_off[r + 1] = lb_off[r] + (2 * lookback_region_bytes(sizes[r]) + 16 + 255) / 256 * 256;
+    if (conc) {
+        B2S_TRY(ctx->seg_lookback.ensure(lb_off[p]));
+        B2S_TRY(ctx->seg_hist.ensure((size_t)p * sizeof(RadixCounters)));
+        B2S_TRY(ctx->seg_plan.ensure((size_t)p * sizeof(RadixPlan)));
+        while ((int)ctx->side.size() < nside) {
+            cudaStream_t st;
+            cudaEvent_t ev;
+            B2S_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            B2S_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            ctx->side.push_back(st);
+            ctx->side_done.push_back(ev);
+        }
+        if (ctx->fork == nullptr) B2S_CUDA(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+        B2S_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
+        for (int i = 0; i < nside; ++i) B2S_CUDA(cudaStreamWaitEvent(ctx->side[i], ctx->fork, 0));
+    }
+    std::vector<const void*> runs;
+    std::vector<const uint32_t*> vruns;
+    std::vector<uint64_t> lens;
+    uint64_t off = 0;
+    const cudaStream_t main = ctx->stream;
+    b2s_status st = B2S_OK;
+    for (int r = 0; r < p && st == B2S_OK; ++r) {
+        const char* src = static_cast<const char*>(din) + off * ksz;
+        char* dst = static_cast<char*>(ctx->seg_keys.ptr) + off * ksz;
+        const uint32_t* vs = dvin ? dvin + off : nullptr;
+        uint32_t* vd = dvin ? static_cast<uint32_t*>(ctx->seg_vals.ptr) + off : nullptr;
+        if (sizes[r] && conc) {
+            SortScratch sc{static_cast<char*>(ctx->alt_keys.ptr) + off * ksz,
+                           dvin ? static_cast<uint32_t*>(ctx->alt_vals.ptr) + off : nullptr,
+                           static_cast<char*>(ctx->seg_lookback.ptr) + lb_off[r],
+                           static_cast<RadixCounters*>(ctx->seg_hist.ptr) + r,
+                           static_cast<RadixPlan*>(ctx->seg_plan.ptr) + r};
+            ctx->stream = ctx->side[r % nside];
+            st = radix_sort(ctx, dtype, src, dst, vs, vd, sizes[r], &sc);
+            ctx->stream = main;
+        } else if (sizes[r]) {
+            st = radix_sort(ctx, dtype, src, dst, vs, vd, sizes[r]);
+        }
+        runs.push_back(dst);
+        vruns.push_back(vd);
+        lens.push_back(sizes[r]);
+        off += sizes[r];
+    }
+    if (conc) {  // join (also on error, so no side stream is left dangling)
+        for (int i = 0; i < nside; ++i) {
+            B2S_CUDA(cudaEventRecord(ctx->side_done[i], ctx->side[i]));
+            B2S_CUDA(cudaStreamWaitEvent(main, ctx->side_done[i], 0));
+        }
+    }
+    B2S_TRY(st);
+    // root merge of the p sorted runs
+    return kway_merge(ctx, dtype, runs.data(), dvin ? vruns.data() : nullptr, lens.data(), p, dout,
+                      dvout, ctx->alt_keys.ptr, static_cast<uint32_t*>(ctx->alt_vals.ptr));
+}
+}  // namespace b2s
+}  // extern "C++"
 
 b2s_status b2s_merge_split_padded(b2s_ctx* ctx, b2s_dtype dtype, const void* mine,
                                   uint64_t n_mine, uint64_t mine_virtuals, const void* theirs,

@@ -124,6 +124,12 @@ struct b2s_ctx {
     void* xbuf_handle_ptr = nullptr;  // allocation the cached handle belongs to
     unsigned char xbuf_handle[64] = {};
     std::map<std::string, void*> peers;  // IPC handle bytes -> mapped pointer
+    // partitioned sort: per-partition scratch and side streams for the
+    // concurrent local sorts
+    b2s::DevBuf seg_lookback, seg_hist, seg_plan;
+    std::vector<cudaStream_t> side;
+    std::vector<cudaEvent_t> side_done;
+    cudaEvent_t fork = nullptr;
 
     bool timing = false;
     cudaEvent_t ev[40] = {};
@@ -150,9 +156,22 @@ inline bool dtype_ok(int t) { return t >= B2S_I32 && t <= B2S_U64; }
 int record(b2s_ctx* ctx);
 void timing_reset(b2s_ctx* ctx);
 
+// The scratch one sort uses; by default the context's own buffers. Several
+// sorts run concurrently (on different streams) each with its own set.
+struct SortScratch {
+    void* alt_keys;          // n keys: ping-pong partner
+    uint32_t* alt_vals;      // n payload words (or null)
+    void* lookback;          // 2 * lookback_region_bytes(n) + 16
+    RadixCounters* ctr;
+    RadixPlan* plan;
+};
+size_t lookback_region_bytes(uint64_t n);
+constexpr int kSideStreams = 8;  // concurrent partition sorts
+
 // device entry points implemented in the .cu files (all async on ctx->stream)
 b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout,
-                      const uint32_t* vin, uint32_t* vout, uint64_t n);
+                      const uint32_t* vin, uint32_t* vout, uint64_t n,
+                      const SortScratch* scratch = nullptr);
 b2s_status kway_merge(b2s_ctx* ctx, b2s_dtype dtype, const void* const* runs,
                       const uint32_t* const* vals, const uint64_t* lens, int k, void* out,
                       uint32_t* vout, void* tmp, uint32_t* vtmp);
@@ -166,6 +185,8 @@ b2s_status select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count, 
 b2s_status bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n, int rank,
                          const b2s_sample* splitters, int nparts, uint64_t* bounds);
 b2s_status probe_lane_order(b2s_ctx* ctx, bool* ok);
+b2s_status partitioned_sort_dev(b2s_ctx* ctx, b2s_dtype dtype, const void* din, void* dout,
+                                const uint32_t* dvin, uint32_t* dvout, uint64_t n, int p);
 b2s_status gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
                     int shift, void* out);
 b2s_status check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,

@@ -1588,6 +1588,8 @@ int onesweep_cfg() {
 // (default 3: an eighth; 64 never). Measured per 2^27-key pass: uniform keys
 // 0.42 ms regular / 0.52 ms hot-digit path; Zipf(1.2) keys, top digit ~20%:
 // 0.557 / 0.525; top digit ~75%: 1.00-1.14 / 0.39-0.48.
+constexpr uint64_t kTwinMinKeys = 1ull << 21;
+
 uint64_t skew_limit(uint64_t n) {
     static int sh = -1;
     if (sh < 0) {
@@ -1657,6 +1659,10 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
 b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
                              void* lb) {
+    // small sorts are bound by the chain of dependent launches, not by the
+    // ranking: one kernel per pass (no skewed / structured twins)
+    if (ctx->atomic_rank && n < kTwinMinKeys)
+        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb);
     if (ctx->atomic_rank)
         return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 2>(ctx, plan, ctr, n, lb);
     return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
@@ -1760,22 +1766,24 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
 
 template <typename U, bool VALS>
 b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kout,
-                        const uint32_t* vin, uint32_t* vout, uint64_t n) {
-    constexpr int TILE = kMinTile;
+                        const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc) {
     constexpr int NP = sizeof(U);
     const uint32_t top_xor = is_signed ? 0x80u : 0u;
-    const uint64_t ntiles = (n + TILE - 1) / TILE;
+    const size_t lb_region = lookback_region_bytes(n);
+    SortScratch own;
+    if (sc == nullptr) {
+        B2S_TRY(ctx->hist.ensure(sizeof(RadixCounters)));
+        B2S_TRY(ctx->alt_keys.ensure(n * sizeof(U)));
+        if (VALS) B2S_TRY(ctx->alt_vals.ensure(n * 4));
+        B2S_TRY(ctx->lookback.ensure(2 * lb_region + 16));
+        B2S_TRY(ctx->plan.ensure(sizeof(RadixPlan)));
+        own = {ctx->alt_keys.ptr, static_cast<uint32_t*>(ctx->alt_vals.ptr), ctx->lookback.ptr,
+               static_cast<RadixCounters*>(ctx->hist.ptr), static_cast<RadixPlan*>(ctx->plan.ptr)};
+        sc = &own;
+    }
+    RadixPlan* plan = sc->plan;
+    RadixCounters* ctr = sc->ctr;
     const bool wide = n >= (1ull << 30);
-    const size_t lb_word = wide ? 8 : 4;
-    const size_t lb_region = ntiles * kRadix * lb_word;
-
-    B2S_TRY(ctx->alt_keys.ensure(n * sizeof(U)));
-    if (VALS) B2S_TRY(ctx->alt_vals.ensure(n * 4));
-    B2S_TRY(ctx->lookback.ensure(2 * lb_region + 16));
-    B2S_TRY(ctx->plan.ensure(sizeof(RadixPlan)));
-    RadixPlan* plan = static_cast<RadixPlan*>(ctx->plan.ptr);
-
-    RadixCounters* ctr = static_cast<RadixCounters*>(ctx->hist.ptr);
     ctx->ev_hist0 = record(ctx);
     B2S_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RadixCounters), ctx->stream));
     {
@@ -1784,13 +1792,12 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
         int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1),
                                            (uint64_t)ctx->num_sms * kPrologueMinBlocks<U>);
         radix_prologue_kernel<U><<<grid, threads, 0, ctx->stream>>>(
-            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(ctx->lookback.ptr),
+            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
             (lb_region + 15) / 16);
         B2S_LAUNCHED();
     }
     radix_plan_kernel<<<1, 32, 0, ctx->stream>>>(plan, ctr, NP, n, top_xor, kin, kout,
-                                                 ctx->alt_keys.ptr, vin, vout,
-                                                 static_cast<uint32_t*>(ctx->alt_vals.ptr));
+                                                 sc->alt_keys, vin, vout, sc->alt_vals);
     B2S_LAUNCHED();
     if (n > 0) {
         int grid = (int)std::min<uint64_t>((n + 511) / 512, (uint64_t)ctx->num_sms * 4);
@@ -1803,9 +1810,9 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
 
     if (n > 0) {
         if (wide)
-            B2S_TRY((launch_passes<U, VALS, unsigned long long>(ctx, plan, ctr, n, ctx->lookback.ptr)));
+            B2S_TRY((launch_passes<U, VALS, unsigned long long>(ctx, plan, ctr, n, sc->lookback)));
         else
-            B2S_TRY((launch_passes<U, VALS, uint32_t>(ctx, plan, ctr, n, ctx->lookback.ptr)));
+            B2S_TRY((launch_passes<U, VALS, uint32_t>(ctx, plan, ctr, n, sc->lookback)));
     }
     {
         int grid = (int)std::min<uint64_t>(std::max<uint64_t>((n + 1023) / 1024, 1),
@@ -1872,17 +1879,21 @@ extern "C" int b2s_debug_phase_cycles(unsigned long long* out16, int reset) {
 }
 #endif
 
+size_t lookback_region_bytes(uint64_t n) {
+    const uint64_t ntiles = (n + kMinTile - 1) / kMinTile;
+    return ntiles * kRadix * (n >= (1ull << 30) ? 8 : 4);
+}
+
 b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout,
-                      const uint32_t* vin, uint32_t* vout, uint64_t n) {
-    B2S_TRY(ctx->hist.ensure(sizeof(RadixCounters)));
+                      const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc) {
     const bool sgn = key_signed(dtype);
     const bool vals = vin != nullptr;
     if (key_bytes(dtype) == 4) {
-        return vals ? radix_sort_t<uint32_t, true>(ctx, sgn, kin, kout, vin, vout, n)
-                    : radix_sort_t<uint32_t, false>(ctx, sgn, kin, kout, vin, vout, n);
+        return vals ? radix_sort_t<uint32_t, true>(ctx, sgn, kin, kout, vin, vout, n, sc)
+                    : radix_sort_t<uint32_t, false>(ctx, sgn, kin, kout, vin, vout, n, sc);
     }
-    return vals ? radix_sort_t<unsigned long long, true>(ctx, sgn, kin, kout, vin, vout, n)
-                : radix_sort_t<unsigned long long, false>(ctx, sgn, kin, kout, vin, vout, n);
+    return vals ? radix_sort_t<unsigned long long, true>(ctx, sgn, kin, kout, vin, vout, n, sc)
+                : radix_sort_t<unsigned long long, false>(ctx, sgn, kin, kout, vin, vout, n, sc);
 }
 
 }  // namespace b2s

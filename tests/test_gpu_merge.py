@@ -135,3 +135,28 @@ def test_merge_empty_runs_with_payload(ctx):
         ok, ov = ctx.merge(runs, vals=vals)
         torch.cuda.synchronize()
         assert torch.equal(ov, torch.cat([x for x in vals]))
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_repeated_calls_see_new_data(ctx, dt):
+    """Repeated device calls on the same buffers (partitioned, out-of-place and
+    in-place sorts) sort the buffers' current contents, also after a larger
+    call reallocated the context's scratch."""
+    rng = np.random.default_rng(11)
+    n, p = 300_001, 4
+    d_in = to_dev(rand_keys(n, dt, rng))
+    d_out = torch.empty_like(d_in)
+    for it in range(6):
+        keys = rand_keys(n, dt, rng, "uniform" if it % 2 else "dups")
+        d_in.copy_(to_dev(keys))
+        ctx.partitioned_sort(d_in, p, out=d_out)
+        s_out, _ = ctx.sort(d_in)  # fresh output each time
+        ctx.sort(d_in, out=d_in)   # in place, same pointers
+        torch.cuda.synchronize()
+        expect = oracle.sort(keys)
+        assert np.array_equal(to_host(d_out, dt), expect), it
+        assert np.array_equal(to_host(d_in, dt), expect), it
+        assert np.array_equal(to_host(s_out, dt), expect), it
+        if it == 3:  # grow every scratch buffer
+            big = to_dev(rand_keys(3 * n, dt, rng))
+            ctx.partitioned_sort(big, p)
