@@ -104,6 +104,12 @@ def ref():
             getattr(lib, f).argtypes = [ctypes.c_int, _p, _p, _p, _p]
         lib.ref_kernel_oracle_cases.argtypes = [ctypes.c_int, _p, _p]
         lib.ref_std_sort.argtypes = [_p, _u64]
+        lib.ref_run_id.argtypes = [ctypes.c_int, _u64, ctypes.c_int, ctypes.c_int, _u64,
+                                   ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+        lib.ref_run_benchmark.argtypes = [ctypes.c_int, _u64, ctypes.c_int, ctypes.c_int, _u64,
+                                          ctypes.c_int, ctypes.c_int] + [ctypes.c_char_p, _u64, _p] * 3
+        lib.ref_run_benchmark.restype = ctypes.c_int
+        lib.ref_to_chars_general.argtypes = [ctypes.c_double, ctypes.c_char_p]
         _ref = lib
     return _ref
 
@@ -253,3 +259,35 @@ def ref_gen_data(n: int, seed: int) -> np.ndarray:
     out = np.empty(n, dtype=np.int64)
     ref().ref_gen_data(n, seed, _ptr(out))
     return out
+
+
+def ref_run_id(algo: str, n: int, procs: int, cores: int, seed: int, mode: str = "wall",
+               reps: int = 1) -> str:
+    """bench::run_id of the reference (P/src/bench.cpp:30-50)."""
+    out = ctypes.create_string_buffer(17)
+    ref().ref_run_id(ALGOS[algo], n, procs, cores, seed, int(mode == "wall"), reps, out)
+    return out.value.decode()
+
+
+def ref_run_benchmark(algo: str, n: int, procs: int, cores: int, seed: int = 1,
+                      mode: str = "wall", reps: int = 1) -> tuple[str, str, str]:
+    """bench::run_benchmark of the reference plus its exports: (experiment-1
+    CSV row, trace JSONL, trace summary JSON)."""
+    caps = [4096, 64 << 20, 1 << 20]
+    bufs = [ctypes.create_string_buffer(c) for c in caps]
+    lens = [ctypes.c_uint64() for _ in caps]
+    args = []
+    for b, c, ln in zip(bufs, caps, lens):
+        args += [b, c, ctypes.addressof(ln)]
+    rc = ref().ref_run_benchmark(ALGOS[algo], n, procs, cores, seed, int(mode == "wall"), reps,
+                                 *args)
+    if rc != 0:
+        raise RuntimeError(f"reference failed: {ref().ref_last_error().decode()}")
+    return tuple(b.value.decode() for b in bufs)
+
+
+def ref_to_chars_general(v: float) -> str:
+    """std::to_chars(general) -- the reference's format_double for finite values."""
+    out = ctypes.create_string_buffer(64)
+    ref().ref_to_chars_general(v, out)
+    return out.value.decode()

@@ -14,6 +14,7 @@
 // P/tests/acceptance.cpp:121-133, P/tests/test_parallel_sort.cpp:330-343) to
 // produce golden fixtures. No reference source is copied here.
 #include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -192,5 +193,61 @@ void ref_kernel_oracle_cases(int count, uint64_t* sizes, int64_t* values) {
 
 // std::sort (the oracle of bench::verify_output, P/src/bench.cpp:97-98).
 void ref_std_sort(int64_t* v, uint64_t n) { std::sort(v, v + n); }
+
+// std::to_chars(general) of a double: what the reference's format_double
+// (P/src/bench.cpp:22-29) prints for finite values.
+void ref_to_chars_general(double v, char* out64) {
+    const auto r = std::to_chars(out64, out64 + 63, v, std::chars_format::general);
+    *r.ptr = 0;
+}
+
+// bench::run_id (P/src/bench.cpp:30-50) of a RunConfig; out gets 16 hex chars + NUL.
+void ref_run_id(int algo, uint64_t n, int procs, int cores, uint64_t seed, int wall, int reps,
+                char* out17) {
+    bench::RunConfig c;
+    c.algorithm = static_cast<parallel::Algorithm>(algo);
+    c.n = n;
+    c.procs = procs;
+    c.cores = cores;
+    c.seed = seed;
+    c.mode = wall ? runtime::Mode::wall : runtime::Mode::counted;
+    c.repetitions = reps;
+    const std::string id = bench::run_id(c);
+    std::memcpy(out17, id.c_str(), 17);
+}
+
+// bench::run_benchmark (P/src/bench.cpp:106-169) of one configuration and its
+// exports: the experiment-1 CSV row (:211-222), the trace JSONL (:335-350)
+// and the trace summary (:352-395). Each output is truncated to its capacity;
+// *_len receives the full length. Returns 0, or -1 (ref_last_error).
+int ref_run_benchmark(int algo, uint64_t n, int procs, int cores, uint64_t seed, int wall, int reps,
+                      char* csv, uint64_t csv_cap, uint64_t* csv_len, char* trace,
+                      uint64_t trace_cap, uint64_t* trace_len, char* summary, uint64_t summary_cap,
+                      uint64_t* summary_len) {
+    try {
+        bench::RunConfig c;
+        c.algorithm = static_cast<parallel::Algorithm>(algo);
+        c.n = n;
+        c.procs = procs;
+        c.cores = cores;
+        c.seed = seed;
+        c.mode = wall ? runtime::Mode::wall : runtime::Mode::counted;
+        c.repetitions = reps;
+        const bench::RunReport r = bench::run_benchmark(c);
+        auto put = [](const std::string& x, char* dst, uint64_t cap, uint64_t* len) {
+            *len = x.size();
+            if (cap == 0) return;
+            const uint64_t k = std::min<uint64_t>(cap - 1, x.size());
+            std::memcpy(dst, x.data(), k);
+            dst[k] = 0;
+        };
+        put(bench::exp1_csv_row(r), csv, csv_cap, csv_len);
+        put(bench::trace_to_jsonl(r), trace, trace_cap, trace_len);
+        put(bench::trace_summary_json(r), summary, summary_cap, summary_len);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e, -1);
+    }
+}
 
 }  // extern "C"

@@ -178,6 +178,34 @@ def main() -> None:
         json.dump(golden, f, indent=0)
     print("wrote", os.path.join(OUT, "golden.json"))
 
+    # report / trace export pins (bench.cpp's run_id, format_double, exp1 row,
+    # trace JSONL and summary): counted mode is bit-deterministic
+    rng = np.random.default_rng(77)
+    ids = []
+    for algo in ("bubble", "merge", "quick"):
+        for n, p, k, seed, mode, reps in [(1 << 20, 4, 4, 1, "wall", 3), (1000, 1, 1, 7, "counted", 1),
+                                          (0, 8, 2, 123, "wall", 1), (1 << 31, 8, 8, 1, "counted", 5)]:
+            ids.append({"algorithm": algo, "n": n, "procs": p, "cores": k, "seed": seed,
+                        "mode": mode, "repetitions": reps,
+                        "run_id": oracle.ref_run_id(algo, n, p, k, seed, mode, reps)})
+    vals = [0.0, -0.0, 1.0, 0.5, 100.0, 1e5, 1e6, 123456.7, 999999.5, 1234567.0, 1e-4, 1e-5,
+            1.25e-5, 3062828.0, 0.213485530554838, 1.0 / 3.0, 2.0e7 / 3.0, 1e21, 5e-324,
+            1.7976931348623157e308, -2.5, -1234567.0]
+    vals += [float(x) for x in rng.uniform(-1e3, 1e3, 40)]
+    vals += [float(10.0 ** e) * float(m) for e, m in zip(rng.integers(-12, 14, 80), rng.uniform(1, 10, 80))]
+    vals += [float(x) for x in rng.integers(0, 1 << 40, 20)]
+    chars = [{"v": repr(v), "s": oracle.ref_to_chars_general(v)} for v in vals]
+    exports = []
+    for algo, n, p, k in [("merge", 4096, 4, 2), ("quick", 3000, 3, 3), ("bubble", 500, 2, 1)]:
+        csv, trace, summary = oracle.ref_run_benchmark(algo, n, p, k, 1, "counted", 1)
+        exports.append({"algorithm": algo, "n": n, "procs": p, "cores": k, "seed": 1,
+                        "mode": "counted", "repetitions": 1, "csv": csv, "trace": trace,
+                        "summary": summary})
+    with open(os.path.join(OUT, "report_golden.json"), "w") as f:
+        json.dump({"generator": "tests/golden/make_golden.py (reference library: oracle/_ref)",
+                   "run_ids": ids, "to_chars": chars, "exports": exports}, f, indent=0)
+    print("wrote", os.path.join(OUT, "report_golden.json"))
+
 
 if __name__ == "__main__":
     main()

@@ -154,3 +154,27 @@ def test_verify_output():
 def test_gen_data_matches_reference(golden):
     for g in golden["gen_data"]:
         assert oracle.fingerprint(sb.gen_data(g["n"], g["seed"])) == int(g["fp"])
+
+
+def test_gpu_run_benchmark_report_and_trace(tmp_path):
+    """bench::run_benchmark's GPU twin: verified report, one compute event per
+    rank plus the root merge, exports in the reference's formats."""
+    import json
+
+    from paper_1105_6040_b200 import report as R
+    rows, reps = R.experiment1(["merge", "quick"], [1 << 16, 5000], [1, 3, 4], [2], seed=3,
+                               repetitions=3)
+    assert len(rows) == 6
+    for row, rep in zip(rows, reps):
+        f = row.split(",")
+        assert f[0] == rep.config.algorithm and int(f[1]) == rep.config.n
+        assert float(f[4]) > 0 and rep.wall_seconds > 0
+        kinds = sorted((e.rank, e.kind) for e in rep.world.trace)
+        assert kinds.count((0, "gather")) == 1
+        assert sum(1 for _, k in kinds if k == "compute") == rep.config.procs
+    path = str(tmp_path / "trace.jsonl")
+    R.emit_trace(reps[2], path)
+    lines = open(path).read().splitlines()
+    assert all(json.loads(l)["run_id"] == R.run_id(reps[2].config) for l in lines)
+    summ = json.load(open(path + ".summary.json"))
+    assert summ["procs"] == 4 and len(summ["ranks"]) == 4
