@@ -254,7 +254,7 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
                       &ctx->lookback, &ctx->hist,      &ctx->plan,      &ctx->parts,
                       &ctx->misc,     &ctx->stage_in,  &ctx->stage_out, &ctx->stage_vin,
                       &ctx->stage_vout, &ctx->xbuf, &ctx->seg_lookback, &ctx->seg_hist,
-                      &ctx->seg_plan};
+                      &ctx->seg_plan, &ctx->kmerge};
     for (cudaStream_t s : ctx->side) cudaStreamDestroy(s);
     for (cudaEvent_t e : ctx->side_done) cudaEventDestroy(e);
     if (ctx->fork) cudaEventDestroy(ctx->fork);

@@ -127,6 +127,7 @@ struct b2s_ctx {
     // partitioned sort: per-partition scratch and side streams for the
     // concurrent local sorts
     b2s::DevBuf seg_lookback, seg_hist, seg_plan;
+    b2s::DevBuf kmerge;  // grouped k-way merge: samples, tags, cuts
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> side_done;
     cudaEvent_t fork = nullptr;

@@ -198,30 +198,52 @@ b2s_status merge2_window(b2s_ctx* ctx, const T* a, const uint32_t* va, uint64_t 
 }
 
 // ---------------------------------------------------------------------------
-// Single-pass k-way merge (k <= kMaxK), replacing ceil(log2 k) pairwise rounds.
+// Grouped k-way merge (3 <= k <= kMaxK): one read and one write per key
+// instead of ceil(log2 k) pairwise rounds.
 //
-// Every S-th element of every run is a boundary record (key, run, position).
-// kmerge_bounds_kernel places each boundary exactly: its cut in every other run
-// is a binary search (ties: lower runs' equal keys come first), its rank among
-// all boundaries is the number of each run's boundaries before those cuts.
-// Between two consecutive boundaries in that order each run contributes at
-// most S elements, so a bucket holds <= k*S keys and fits in shared memory.
-// kmerge_bucket_kernel loads each bucket's k sub-ranges with coalesced reads,
-// merges them pairwise in shared memory (log2 k rounds, stable: ties to the
-// lower run) and writes the bucket with coalesced stores at its output offset
-// (the sum of its lower cuts). HBM traffic: one read + one write per key.
+// 1. Every S-th element of every run becomes a sample (key, run << 26 | chunk);
+//    the samples are radix-sorted as pairs (stable: equal keys stay in run
+//    order), which is the order of the samples in the merged output.
+// 2. Every (T/S)-th sorted sample closes a group. Its cut in its own run is its
+//    position + 1; in a lower run the elements <= its key come before it (ties
+//    go to lower runs), in a higher run those < its key. A group then holds at
+//    most S more elements per run than its T/S samples account for:
+//    <= T + k*S keys (GroupSmem::CAP).
+// 3. One CTA per group loads its k slices into shared memory (cp.async),
+//    merges them pairwise in shared memory (log2 k rounds, ties to the lower
+//    run, two heads in registers) and writes the group at its output offset
+//    (the sum of its lower cuts) with coalesced stores.
 
 constexpr int kMaxK = 16;
+constexpr int kKThreads = 256;
+
+template <typename T>
+struct GroupCfg {
+    static constexpr uint32_t S = sizeof(T) == 4 ? 256 : 128;   // sample stride
+    static constexpr uint32_t T_ = sizeof(T) == 4 ? 4096 : 2048; // group target
+};
 
 template <typename T>
 struct KRuns {
     const T* key[kMaxK];
     const uint32_t* val[kMaxK];
     uint64_t n[kMaxK];
-    uint64_t nb_off[kMaxK + 1];  // prefix of boundaries per run
+    uint64_t soff[kMaxK + 1];  // prefix of samples per run
     int k;
-    uint32_t S;                   // boundary stride
 };
+
+template <typename T>
+__global__ void kmerge_samples_kernel(const KRuns<T> R, T* __restrict__ skeys,
+                                      uint32_t* __restrict__ stags) {
+    constexpr uint32_t S = GroupCfg<T>::S;
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= R.soff[R.k]) return;
+    int r = 0;
+    while (q >= R.soff[r + 1]) ++r;
+    const uint64_t c = q - R.soff[r];
+    skeys[q] = R.key[r][c * S + S - 1];
+    stags[q] = ((uint32_t)r << 26) | (uint32_t)c;
+}
 
 template <typename T>
 __device__ __forceinline__ uint64_t bound_in(const T* a, uint64_t n, T v, bool upper) {
@@ -235,171 +257,237 @@ __device__ __forceinline__ uint64_t bound_in(const T* a, uint64_t n, T v, bool u
     return lo;
 }
 
+// cuts[(g + 1) * k + r]: run r's cut at the end of group g; row 0 is zeros and
+// the last row the run lengths
 template <typename T>
-__global__ void kmerge_bounds_kernel(const KRuns<T> R, uint64_t* __restrict__ cuts) {
-    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (q >= R.nb_off[R.k]) return;
-    int r = 0;
-    while (q >= R.nb_off[r + 1]) ++r;
-    const uint64_t j = q - R.nb_off[r];
-    const uint64_t pos = (j + 1) * R.S - 1;
-    const T v = R.key[r][pos];
-    uint64_t c[kMaxK];
-    uint64_t rank = j;
-    for (int r2 = 0; r2 < R.k; ++r2) {
-        uint64_t cut;
+__global__ void kmerge_cuts_kernel(const KRuns<T> R, const T* __restrict__ skeys,
+                                   const uint32_t* __restrict__ stags, uint64_t ngroups,
+                                   uint32_t per_group, uint64_t* __restrict__ cuts) {
+    constexpr uint32_t S = GroupCfg<T>::S;
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const int k = R.k;
+    if (t >= (ngroups + 1) * k) return;
+    const uint64_t g = t / k;  // boundary row
+    const int r2 = (int)(t % k);
+    uint64_t cut;
+    if (g == 0) {
+        cut = 0;
+    } else if (g == ngroups) {
+        cut = R.n[r2];
+    } else {
+        const uint64_t j = g * per_group - 1;  // closing sample of group g-1
+        const T v = skeys[j];
+        const int r = (int)(stags[j] >> 26);
+        const uint64_t pos = (uint64_t)(stags[j] & ((1u << 26) - 1)) * S + S - 1;
         if (r2 == r) cut = pos + 1;
         else cut = bound_in(R.key[r2], R.n[r2], v, r2 < r);
-        c[r2] = cut;
-        if (r2 != r) rank += cut / R.S;
     }
-    for (int r2 = 0; r2 < R.k; ++r2) cuts[rank * R.k + r2] = c[r2];
+    cuts[g * k + r2] = cut;
 }
 
-constexpr int kKThreads = 256;
+// shared bytes of a group kernel for k runs: two buffers of cap records
+template <typename T, bool VALS>
+constexpr uint32_t group_cap(int k) {
+    return GroupCfg<T>::T_ + (uint32_t)k * GroupCfg<T>::S + 4;  // + one-past-the-end read
+}
+template <typename T, bool VALS>
+constexpr size_t group_smem(uint32_t cap) {
+    return 2 * (size_t)cap * sizeof(T) + (VALS ? 2 * (size_t)cap * 4 : 0);
+}
 
 template <typename T, bool VALS>
-__global__ void __launch_bounds__(kKThreads) kmerge_bucket_kernel(const KRuns<T> R,
-                                                                  const uint64_t* __restrict__ cuts,
-                                                                  uint64_t nbuckets, uint32_t per_cta,
-                                                                  uint32_t cap, T* __restrict__ out,
-                                                                  uint32_t* __restrict__ vout) {
+__global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> R,
+                                                                 const uint64_t* __restrict__ cuts,
+                                                                 uint32_t cap, T* __restrict__ out,
+                                                                 uint32_t* __restrict__ vout) {
+    constexpr int ITEMS = sizeof(T) == 4 ? 19 : 15;  // odd: conflict-free strided stores
     extern __shared__ __align__(16) unsigned char smem[];
-    T* kA = reinterpret_cast<T*>(smem);
-    T* kB = kA + cap;
-    uint32_t* vA = reinterpret_cast<uint32_t*>(kB + cap);
-    uint32_t* vB = vA + (VALS ? cap : 0);
+    // buffers are selected arithmetically (an indexed pointer array would
+    // lose the shared address space and turn every access generic)
+    T* const kbase = reinterpret_cast<T*>(smem);
+    uint32_t* const vbase = reinterpret_cast<uint32_t*>(smem + 2 * (size_t)cap * sizeof(T));
+    __shared__ uint32_t s_seg[kMaxK + 1];
     __shared__ uint64_t s_lo[kMaxK];
-    __shared__ uint32_t s_seg[kMaxK + 1];  // segment offsets inside the bucket
     __shared__ uint64_t s_out;
     const int k = R.k;
     const int tid = threadIdx.x;
-    const uint64_t b0 = (uint64_t)blockIdx.x * per_cta;
-    const uint64_t b1 = b0 + per_cta < nbuckets ? b0 + per_cta : nbuckets;
-    for (uint64_t b = b0; b < b1; ++b) {
-        if (tid == 0) {
-            uint32_t acc = 0;
-            uint64_t o = 0;
-            for (int r = 0; r < k; ++r) {
-                const uint64_t lo = b == 0 ? 0 : cuts[(b - 1) * k + r];
-                const uint64_t hi = b + 1 == nbuckets ? R.n[r] : cuts[b * k + r];
-                s_lo[r] = lo;
-                s_seg[r] = acc;
-                acc += (uint32_t)(hi - lo);
-                o += lo;
-            }
-            s_seg[k] = acc;
-            s_out = o;
-        }
-        __syncthreads();
-        const uint32_t total = s_seg[k];
-        // coalesced loads of the k sub-ranges, concatenated in run order
+    const uint64_t g = blockIdx.x;
+    if (tid == 0) {
+        uint32_t acc = 0;
+        uint64_t o = 0;
         for (int r = 0; r < k; ++r) {
-            const uint32_t base = s_seg[r], len = s_seg[r + 1] - base;
-            const T* src = R.key[r] + s_lo[r];
-            for (uint32_t i = tid; i < len; i += kKThreads) kA[base + i] = src[i];
-            if constexpr (VALS) {
-                const uint32_t* vs = R.val[r] + s_lo[r];
-                for (uint32_t i = tid; i < len; i += kKThreads) vA[base + i] = vs[i];
-            }
+            const uint64_t lo = cuts[g * k + r], hi = cuts[(g + 1) * k + r];
+            s_lo[r] = lo;
+            s_seg[r] = acc;
+            acc += (uint32_t)(hi - lo);
+            o += lo;
         }
-        __syncthreads();
-        // pairwise rounds in shared memory; a pair keeps the position range of
-        // its two segments, so segment offsets after a round are every other one
-        T* ka = kA;
-        T* kb = kB;
-        uint32_t* va = vA;
-        uint32_t* vb = vB;
-        int nseg = k;
-        int stride = 1;  // segments of this round start at s_seg[i * stride]
-        while (nseg > 1) {
-            constexpr int ITEMS = 8;
-            for (uint32_t x0 = tid * ITEMS; x0 < total; x0 += kKThreads * ITEMS) {
-                const uint32_t x1 = x0 + ITEMS < total ? x0 + ITEMS : total;
-                uint32_t x = x0;
-                while (x < x1) {
-                    // the pair holding output position x
-                    int pr = 0;
-                    while (pr + 1 < (nseg + 1) / 2 && s_seg[min((pr + 1) * 2 * stride, k)] <= x) ++pr;
-                    const uint32_t a0 = s_seg[min(pr * 2 * stride, k)];
-                    const uint32_t a1 = s_seg[min(pr * 2 * stride + stride, k)];
-                    const uint32_t e1 = s_seg[min(pr * 2 * stride + 2 * stride, k)];
-                    const uint32_t la = a1 - a0, lb = e1 - a1;
-                    const uint32_t diag = x - a0;
-                    uint32_t ai = merge_path_smem(ka + a0, la, ka + a1, lb, diag);
-                    uint32_t bi = diag - ai;
-                    const uint32_t stop = x1 < e1 ? x1 : e1;
-                    for (; x < stop; ++x) {
-                        const bool take_a = bi >= lb || (ai < la && !(ka[a1 + bi] < ka[a0 + ai]));
-                        const uint32_t src = take_a ? a0 + ai++ : a1 + bi++;
-                        kb[x] = ka[src];
-                        if constexpr (VALS) vb[x] = va[src];
+        s_seg[k] = acc;
+        s_out = o;
+    }
+    __syncthreads();
+    const uint32_t total = s_seg[k];
+    // the k slices, concatenated in run order
+    for (int r = 0; r < k; ++r) {
+        const uint32_t base = s_seg[r], len = s_seg[r + 1] - base;
+        const T* src = R.key[r] + s_lo[r];
+        for (uint32_t i = tid; i < len; i += kKThreads) cp_async_elem(&kbase[base + i], src + i);
+        if constexpr (VALS) {
+            const uint32_t* vs = R.val[r] + s_lo[r];
+            for (uint32_t i = tid; i < len; i += kKThreads) cp_async_elem(&vbase[base + i], vs + i);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // pairwise rounds in shared memory; after a round segment i spans the old
+    // segments 2i and 2i+1
+    int cur = 0;
+    int m = k;
+    while (m > 1) {
+        const T* ks = kbase + (cur ? cap : 0);
+        T* kd = kbase + (cur ? 0 : cap);
+        const uint32_t* vs = vbase + (cur ? cap : 0);
+        uint32_t* vd = vbase + (cur ? 0 : cap);
+        for (uint32_t x0 = tid * ITEMS; x0 < total; x0 += kKThreads * ITEMS) {
+            const uint32_t x1 = min(x0 + ITEMS, total);
+            uint32_t x = x0;
+            int p = 0;
+            while (2 * (p + 1) < m && s_seg[2 * (p + 1)] <= x) ++p;  // pair holding x
+            {
+                // common case: the whole chunk inside one pair, fully unrolled
+                const uint32_t a0 = s_seg[2 * p];
+                const uint32_t a1 = s_seg[min(2 * p + 1, m)];
+                const uint32_t e1 = s_seg[min(2 * p + 2, m)];
+                if (x0 + ITEMS <= e1) {
+                    const uint32_t diag = x0 - a0;
+                    uint32_t ai = a0 + merge_path_smem(ks + a0, a1 - a0, ks + a1, e1 - a1, diag);
+                    uint32_t bi = a1 + (diag - (ai - a0));
+                    T ka = ks[ai], kb = ks[bi];
+#pragma unroll
+                    for (int j = 0; j < ITEMS; ++j) {
+                        const bool take_a = bi >= e1 || (ai < a1 && !(kb < ka));
+                        kd[x0 + j] = take_a ? ka : kb;
+                        if constexpr (VALS) vd[x0 + j] = vs[take_a ? ai : bi];
+                        const uint32_t nxt = take_a ? ++ai : ++bi;
+                        const T kn = ks[nxt];
+                        if (take_a) ka = kn;
+                        else kb = kn;
                     }
+                    continue;
                 }
             }
-            __syncthreads();
-            T* t = ka;
-            ka = kb;
-            kb = t;
-            uint32_t* tv = va;
-            va = vb;
-            vb = tv;
-            nseg = (nseg + 1) / 2;
-            stride *= 2;
-        }
-        const uint64_t o = s_out;
-        for (uint32_t i = tid; i < total; i += kKThreads) {
-            out[o + i] = ka[i];
-            if constexpr (VALS) vout[o + i] = va[i];
+            while (x < x1) {
+                const uint32_t a0 = s_seg[2 * p];
+                const uint32_t a1 = s_seg[min(2 * p + 1, m)];
+                const uint32_t e1 = s_seg[min(2 * p + 2, m)];
+                const uint32_t diag = x - a0;
+                uint32_t ai = a0 + merge_path_smem(ks + a0, a1 - a0, ks + a1, e1 - a1, diag);
+                uint32_t bi = a1 + (diag - (ai - a0));
+                T ka = ks[ai], kb = ks[bi];
+                const uint32_t stop = min(x1, e1);
+                for (; x < stop; ++x) {
+                    const bool take_a = bi >= e1 || (ai < a1 && !(kb < ka));
+                    kd[x] = take_a ? ka : kb;
+                    if constexpr (VALS) vd[x] = vs[take_a ? ai : bi];
+                    const uint32_t nxt = take_a ? ++ai : ++bi;
+                    const T kn = ks[nxt];
+                    if (take_a) ka = kn;
+                    else kb = kn;
+                }
+                ++p;
+            }
         }
         __syncthreads();
+        if (tid == 0) {
+            const int m2 = (m + 1) / 2;
+            for (int i = 1; i <= m2; ++i) s_seg[i] = s_seg[min(2 * i, m)];
+        }
+        m = (m + 1) / 2;
+        cur ^= 1;
+        __syncthreads();
+    }
+    const uint64_t o = s_out;
+    const T* kf = kbase + (cur ? cap : 0);
+    const uint32_t* vf = vbase + (cur ? cap : 0);
+    for (uint32_t i = tid; i < total; i += kKThreads) {
+        __stcs(out + o + i, kf[i]);
+        if constexpr (VALS) __stcs(vout + o + i, vf[i]);
     }
 }
 
+template <typename T> constexpr b2s_dtype dtype_of();
+template <> constexpr b2s_dtype dtype_of<int32_t>() { return B2S_I32; }
+template <> constexpr b2s_dtype dtype_of<uint32_t>() { return B2S_U32; }
+template <> constexpr b2s_dtype dtype_of<int64_t>() { return B2S_I64; }
+template <> constexpr b2s_dtype dtype_of<unsigned long long>() { return B2S_U64; }
+
+template <typename T, bool VALS>
+b2s_status launch_groups(b2s_ctx* ctx, const KRuns<T>& R, const uint64_t* cuts, uint64_t ngroups,
+                         T* out, uint32_t* vout) {
+    auto kern = kmerge_group_kernel<T, VALS>;
+    static bool init = false;
+    if (!init) {
+        B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)group_smem<T, VALS>(group_cap<T, VALS>(kMaxK))));
+        init = true;
+    }
+    const uint32_t cap = group_cap<T, VALS>(R.k);
+    kern<<<(unsigned)ngroups, kKThreads, group_smem<T, VALS>(cap), ctx->stream>>>(R, cuts, cap, out, vout);
+    B2S_LAUNCHED();
+    return B2S_OK;
+}
+
+// sample tags hold a 26-bit chunk index
 template <typename T>
-b2s_status kway_single_pass(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* vals,
-                            const uint64_t* lens, int k, void* out, uint32_t* vout) {
+bool kway_grouped_fits(const uint64_t* lens, int k) {
+    for (int r = 0; r < k; ++r)
+        if (lens[r] / GroupCfg<T>::S >= (1ull << 26)) return false;
+    return true;
+}
+
+template <typename T>
+b2s_status kway_grouped(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* vals,
+                        const uint64_t* lens, int k, void* out, uint32_t* vout) {
+    constexpr uint32_t S = GroupCfg<T>::S;
+    constexpr uint32_t per_group = GroupCfg<T>::T_ / S;
     const bool with_vals = vout != nullptr;
-    const size_t rec = sizeof(T) + (with_vals ? 4 : 0);
-    // two buffers of `cap` records in <= 64 KB, cap = k * S with S a power of two
-    uint32_t S = 1;
-    const char* es = getenv("B2S_KWAY_SMEM_KB");
-    const uint64_t budget = (uint64_t)(es ? atoi(es) : 64) * 1024;
-    while ((uint64_t)2 * k * (S * 2) * rec <= budget) S *= 2;
-    const uint32_t cap = (uint32_t)k * S;
     KRuns<T> R{};
     R.k = k;
-    R.S = S;
-    R.nb_off[0] = 0;
-    uint64_t total = 0;
+    R.soff[0] = 0;
     for (int r = 0; r < k; ++r) {
         R.key[r] = static_cast<const T*>(runs[r]);
         R.val[r] = with_vals ? vals[r] : nullptr;
         R.n[r] = lens[r];
-        R.nb_off[r + 1] = R.nb_off[r] + lens[r] / S;
-        total += lens[r];
+        R.soff[r + 1] = R.soff[r] + lens[r] / S;
     }
-    const uint64_t nb = R.nb_off[k];
-    const uint64_t nbuckets = nb + 1;
-    B2S_TRY(ctx->parts.ensure((nb * k + 1) * sizeof(uint64_t)));
-    uint64_t* cuts = static_cast<uint64_t*>(ctx->parts.ptr);
+    const uint64_t m = R.soff[k];
+    const uint64_t ngroups = m / per_group + 1;
+    // scratch: samples (in, sorted), tags (in, sorted), cuts
+    const size_t sk = (m * sizeof(T) + 255) / 256 * 256, st = (m * 4 + 255) / 256 * 256;
+    const size_t cb = (ngroups + 1) * k * sizeof(uint64_t);
+    B2S_TRY(ctx->kmerge.ensure(2 * sk + 2 * st + cb + 256));
+    char* base = static_cast<char*>(ctx->kmerge.ptr);
+    T* s_in = reinterpret_cast<T*>(base);
+    T* s_out = reinterpret_cast<T*>(base + sk);
+    uint32_t* t_in = reinterpret_cast<uint32_t*>(base + 2 * sk);
+    uint32_t* t_out = reinterpret_cast<uint32_t*>(base + 2 * sk + st);
+    uint64_t* cuts = reinterpret_cast<uint64_t*>(base + 2 * sk + 2 * st);
     ctx->ev_merge0 = record(ctx);
-    if (nb > 0) {
-        kmerge_bounds_kernel<T><<<(unsigned)((nb + 255) / 256), 256, 0, ctx->stream>>>(R, cuts);
+    if (m > 0) {
+        kmerge_samples_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, ctx->stream>>>(R, s_in, t_in);
         B2S_LAUNCHED();
+        B2S_TRY(radix_sort(ctx, dtype_of<T>(), s_in, s_out, t_in, t_out, m));
     }
-    const size_t smem = (size_t)2 * cap * rec;
-    auto kern = with_vals ? kmerge_bucket_kernel<T, true> : kmerge_bucket_kernel<T, false>;
-    B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const uint64_t want_ctas = (uint64_t)ctx->num_sms * 3 * 4;
-    const uint32_t per_cta = (uint32_t)std::max<uint64_t>(1, (nbuckets + want_ctas - 1) / want_ctas);
-    const unsigned grid = (unsigned)((nbuckets + per_cta - 1) / per_cta);
-    kern<<<grid, kKThreads, smem, ctx->stream>>>(R, cuts, nbuckets, per_cta, cap,
-                                                 static_cast<T*>(out), vout);
+    const uint64_t nc = (ngroups + 1) * k;
+    kmerge_cuts_kernel<T><<<(unsigned)((nc + 255) / 256), 256, 0, ctx->stream>>>(R, s_out, t_out, ngroups,
+                                                                                per_group, cuts);
     B2S_LAUNCHED();
+    if (with_vals)
+        B2S_TRY((launch_groups<T, true>(ctx, R, cuts, ngroups, static_cast<T*>(out), vout)));
+    else
+        B2S_TRY((launch_groups<T, false>(ctx, R, cuts, ngroups, static_cast<T*>(out), vout)));
     ctx->ev_merge1 = record(ctx);
     ctx->last_merge_rounds = 1;
-    (void)total;
     return B2S_OK;
 }
 
@@ -427,8 +515,8 @@ b2s_status kway_t(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* 
                   const uint64_t* lens, int k, void* out, uint32_t* vout, void* tmp,
                   uint32_t* vtmp) {
     const bool with_vals = vout != nullptr;
-    if (k > 2 && k <= kMaxK && kway_mode() == 1)
-        return kway_single_pass<T>(ctx, runs, vals, lens, k, out, vout);
+    if (k > 2 && k <= kMaxK && kway_mode() == 1 && kway_grouped_fits<T>(lens, k))
+        return kway_grouped<T>(ctx, runs, vals, lens, k, out, vout);
     std::vector<Run> cur;
     uint64_t total = 0;
     for (int i = 0; i < k; ++i) {
