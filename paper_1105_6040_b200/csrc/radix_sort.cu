@@ -305,6 +305,12 @@ __global__ void __launch_bounds__(512) radix_fallback_hist_kernel(const RadixPla
 #define B2S_MATCH_HYBRID 2
 #endif
 constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
+#ifndef B2S_ERANK
+#define B2S_ERANK 1
+#endif
+#ifndef B2S_ERANK_RELOAD
+#define B2S_ERANK_RELOAD 1
+#endif
 //
 // Shared-memory traffic is this kernel's bound on B200 (HBM is 6.5 TB/s but
 // the random-access shared memory work per key is ~15-20 wavefronts per 32
@@ -532,7 +538,11 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                                               long long& prof_t, uint32_t hot = 0) {
     // RANK: 0 ballot matching, 1 lane-ordered atomics, 2 atomics except for
     // the pass's hot digit, whose lanes are counted and ranked by one ballot
-    // per row against a warp-uniform running count (skewed passes)
+    // per row against a warp-uniform running count (skewed passes), 5 the
+    // early count's atomics return the in-warp ranks (lane-ordered, packed
+    // 16-bit counters) and ranking is one lookup of the warp's digit base --
+    // for full TMA-landed tiles; other tiles rank as 1
+    constexpr bool ER = RANK == 5 && FULL && FROM_SMEM && !PIPE;
     (void)prof_acc;
     (void)prof_t;
     (void)hot;
@@ -557,6 +567,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // lane l is key j*32+l (coalesced / conflict-free; in-warp order == input order)
     U keys[ITEMS];
     uint32_t vals[VALS ? ITEMS : 1];
+    uint32_t rr[ER ? (ITEMS + 1) / 2 : 1];  // RANK 5: packed in-warp ranks
     const uint32_t wbase = warp * WSEG;
     if constexpr (FROM_SMEM) {
 #pragma unroll
@@ -606,6 +617,33 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             if (valid && !is_hot) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
         }
         if (lane == 0 && hot_n) atomicAdd(ecnt + ((hot & 1) * HALF + (hot >> 1)), hot_n);
+    } else if constexpr (ER) {
+        // in-warp ranks: item j of lane l precedes item j of lane l+1 and item
+        // j+1 of every lane, and same-word lanes of one atomic are served in
+        // lane order (b2s::probe_lane_order), so the old value is the rank
+        const uint32_t ecnt_a = smem_addr(ecnt);
+        constexpr int B = 4;
+#pragma unroll
+        for (int j0 = 0; j0 < ITEMS; j0 += B) {
+            uint32_t old[B], s16[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (j0 + b < ITEMS) {
+                    const uint32_t d = digit_of(keys[j0 + b], shift, dxor);
+                    s16[b] = 16 * (d & 1);
+                    old[b] = atom_add_shared(ecnt_a + 4 * (d >> 1), 1u << s16[b]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int j = j0 + b;
+                if (j < ITEMS) {
+                    const uint32_t r = (old[b] >> s16[b]) & 0xFFFFu;
+                    if (j & 1) rr[j >> 1] |= r << 16;
+                    else rr[j >> 1] = r;
+                }
+            }
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
@@ -623,9 +661,14 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #pragma unroll 4
         for (int w = 0; w < WARPS; ++w) {
             uint32_t* e = s_early + w * kRadix;
-            const uint32_t c = e[tid] | (e[HALF + tid] << 16);
-            e[tid] = 0;
-            e[HALF + tid] = 0;
+            uint32_t c;
+            if constexpr (ER) {
+                c = e[tid];  // packed pair; the region is cleared at the next tile's start
+            } else {
+                c = e[tid] | (e[HALF + tid] << 16);
+                e[tid] = 0;
+                e[HALF + tid] = 0;
+            }
             s_cnt[w * HALF + tid] = pair;
             pair += c;
         }
@@ -670,6 +713,20 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         for (int w = 0; w < WARPS; ++w) s_cnt[w * HALF + tid] += add;
     }
     __syncthreads();
+#if B2S_ERANK_RELOAD
+    if constexpr (ER) {
+        // only the packed ranks were held across the digit section; the keys
+        // come back from the landing buffer, and the in-place scatter starts
+        // once every warp holds them
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) keys[j] = kbuf[wbase + j * 32 + lane];
+        if constexpr (VALS) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) vals[j] = vbuf[wbase + j * 32 + lane];
+        }
+        __syncthreads();
+    }
+#endif
     B2S_PHASE(2);
 
     // ---- rank within the tile and stage digit-sorted in shared memory. The
@@ -678,7 +735,18 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // ranks are stable. The highest lane of each digit group claims the group's
     // slots with one atomic and shuffles the base to its peers.
     const uint32_t lanemask_lt = (1u << lane) - 1u;
-    if constexpr (RANK == 2 && FULL) {
+    if constexpr (ER) {
+        // slot = tile start of the digit + this warp's prefix (s_cnt, packed)
+        // + the in-warp rank
+        const uint32_t* wc = s_cnt + warp * HALF;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t d = digit_of(keys[j], shift, dxor);
+            const uint32_t r = ((wc[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + ((rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+            sts_key(keys_a + swz<sizeof(U), SWZ>(r) * (uint32_t)sizeof(U), keys[j]);
+            if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(r), vals[j]);
+        }
+    } else if constexpr (RANK == 2 && FULL) {
         // hot lanes: the warp's running offset of the hot digit (nobody
         // else touches its counter) plus the lanes below in this row
         uint32_t hot_run = (s_cnt[warp * HALF + (hot >> 1)] >> (16 * (hot & 1))) & 0xFFFFu;
@@ -708,7 +776,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                 }
             }
         }
-    } else if constexpr (RANK == 1 && FULL) {
+    } else if constexpr ((RANK == 1 || RANK == 5) && FULL) {
         // atomic ranking in batches of 4 items: the batch's atomics are
         // independent (the warp's shared accesses stay in program order, so
         // the counters advance exactly as item by item) and their latencies
@@ -860,9 +928,12 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     B2S_PHASE(4);
     claim_next();
 
-    // ---- write runs of equal digits; clear this warp's counters
+    // ---- write runs of equal digits; clear this warp's counters (RANK 5
+    // overwrites them in the digit section)
+    if constexpr (!ER) {
 #pragma unroll
-    for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
+        for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
+    }
     writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2, SWZ>(kbuf, vbuf, gbase_out, tile_valid, dst,
                                                                vdst, shift, dxor, nd);
 }
@@ -879,6 +950,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     constexpr int TILE = SM::TILE;
     static_assert(THREADS >= kRadix, "one thread per digit is required");
     static_assert(TILE < 65536, "packed 16-bit warp counters");
+    // Full tiles of RANK 1, 2 and 4 rank by the early count's returned in-warp
+    // ranks plus one lookup (onesweep_tile RANK 5; B2S_ERANK=0 restores the
+    // second atomic pass: 0.811 -> 0.774 ms per 2^28-key u32 pass).
     // RANK: 0 ballots, 1 atomics (one kernel per pass), or one of three
     // kernels launched back to back per pass, exactly one of which runs it:
     //   2  atomics, unless the pass is skewed or the input structured;
@@ -890,7 +964,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     // take the SMs as the predecessor's drain, and the ones not suited to the
     // pass exit at once. What they decide on (the pass's histogram, the
     // prologue's order statistic) was final before 2 started.
-    constexpr int TR = RANK == 3 ? 2 : (RANK >= 2 ? 1 : RANK);
+    constexpr int TR = RANK == 3 ? 2 : (RANK >= 1 ? (B2S_ERANK ? 5 : 1) : 0);
     constexpr bool SWZ = RANK == 4;
     if constexpr (RANK == 2 || RANK == 3)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1766,6 +1840,13 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
     // tuning alternatives (B2S_ONESWEEP_CFG), kept with their measured results
     // in DESIGN.md.
     const int cfg = onesweep_cfg();
+#ifdef B2S_DEV_FAST
+    // development builds (tools/kdev_build.sh, -DB2S_DEV_FAST): only the default
+    // u32 keys-only pass is compiled, for quick kernel iteration
+    (void)cfg;
+    if constexpr (sizeof(U) == 4 && !VALS) return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
+    return B2S_EINVAL;
+#else
     if constexpr (sizeof(U) == 4 && VALS) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
@@ -1787,6 +1868,7 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     }
+#endif
 }
 
 template <typename U, bool VALS>
