@@ -308,6 +308,9 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_ERANK
 #define B2S_ERANK 1
 #endif
+#ifndef B2S_SEP
+#define B2S_SEP 1
+#endif
 #ifndef B2S_ERANK_RELOAD
 #define B2S_ERANK_RELOAD 1
 #endif
@@ -523,7 +526,7 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
-          bool PIPE, int RANK, bool SWZ = false, typename Claim, typename Between>
+          bool PIPE, int RANK, bool SWZ = false, bool SEP = false, typename Claim, typename Between>
 __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Between& between,
                                               typename TileShared<LB>::OFF* gbase_out, uint32_t tile,
                                               uint32_t tile_valid, uint64_t tile_base,
@@ -532,6 +535,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                                               uint32_t* __restrict__ vdst, LB* __restrict__ lb_cur,
                                               int shift, uint32_t dxor, const NextDigit nd,
                                               uint32_t* s_cnt, U* kbuf, uint32_t* vbuf,
+                                              U* sbuf, uint32_t* svbuf,
                                               uint32_t* s_match, uint32_t* s_early,
                                               TileShared<LB>& sh,
                                               unsigned long long* prof_acc,
@@ -557,8 +561,10 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const uint32_t cnt_a = smem_addr(s_cnt + warp * HALF);
-    const uint32_t keys_a = smem_addr(kbuf);
-    const uint32_t vals_a = smem_addr(vbuf);
+    // staging (scatter) target: the landing buffer itself, or with SEP the
+    // other tile buffer (then the landing buffer is only ever read here)
+    const uint32_t keys_a = smem_addr(sbuf);
+    const uint32_t vals_a = smem_addr(svbuf);
     const uint32_t match_a = smem_addr(s_match + warp * kRadix);
     (void)match_a;
     const uint32_t dummy_a = smem_addr(sh.dummy + lane);
@@ -724,7 +730,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #pragma unroll
             for (int j = 0; j < ITEMS; ++j) vals[j] = vbuf[wbase + j * 32 + lane];
         }
-        __syncthreads();
+        if constexpr (!SEP) __syncthreads();  // in-place staging: all reads first
     }
 #endif
     B2S_PHASE(2);
@@ -934,7 +940,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #pragma unroll
         for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
     }
-    writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2, SWZ>(kbuf, vbuf, gbase_out, tile_valid, dst,
+    writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2, SWZ>(sbuf, svbuf, gbase_out, tile_valid, dst,
                                                                vdst, shift, dxor, nd);
 }
 
@@ -965,6 +971,10 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     // pass exit at once. What they decide on (the pass's histogram, the
     // prologue's order statistic) was final before 2 started.
     constexpr int TR = RANK == 3 ? 2 : (RANK >= 1 ? (B2S_ERANK ? 5 : 1) : 0);
+    // separate landing / staging buffers: measured per 2^28-key u32 pass,
+    // uniform keys 0.776 ms in place vs 0.794 separate, ascending (the
+    // structured twin) 0.709 vs 0.699 -- so only the structured twin uses it
+    constexpr bool SEP = TR == 5 && RANK == 4 && B2S_SEP;
     constexpr bool SWZ = RANK == 4;
     if constexpr (RANK == 2 || RANK == 3)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1097,33 +1107,38 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         // this tile) but published and prefetched only after the look-back
         uint32_t next_t = 0;
         if (tid == THREADS - 1) next_t = atomicAdd(&plan->tile_counter[slot], 1u);
+        // SEP: tiles always land in buffer 0 and are staged in buffer 1
+        // (which also holds the early counts); else the two alternate and
+        // each tile is staged in place
+        const int lb_ = SEP ? 0 : cur;
+        const int sb_ = SEP ? 1 : cur;
         auto claim = [&]() {
             if (tid == THREADS - 1) {
                 sh.tile[cur ^ 1] = next_t;
-                prefetch(next_t, cur ^ 1);
+                prefetch(next_t, SEP ? 0 : cur ^ 1);
             }
         };
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
         if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
-        uint32_t* idle = reinterpret_cast<uint32_t*>(kbuf[cur ^ 1]);
+        uint32_t* idle = reinterpret_cast<uint32_t*>(kbuf[SEP ? 1 : cur ^ 1]);
         if (rem >= (uint64_t)TILE) {
             if (tma) {
-                mbar_wait(mbar_a[cur], (parity >> cur) & 1u);
-                parity ^= 1u << cur;
+                mbar_wait(mbar_a[lb_], (parity >> lb_) & 1u);
+                parity ^= 1u << lb_;
                 B2S_PHASE(0);
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR, SWZ>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR, SWZ, SEP>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
+                    s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR, SWZ>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR, SWZ, SEP>(
                     claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
+                    s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR, SWZ>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR, SWZ, SEP>(
                 claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
-                nd, s_cnt, kbuf[cur], vbuf[cur], idle, idle, sh, prof_acc, prof_t, hot);
+                nd, s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
         }
         __syncthreads();
         B2S_PHASE(5);
@@ -1281,19 +1296,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan*
                 parity ^= 1u << cur;
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true, RANK>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
-                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
+                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true, RANK>(
                     noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
-                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
+                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                     prof_t);
             }
             prev_valid = TILE;
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true, RANK>(
                 noop, write_prev, s_gbase2[gcur], tile, (uint32_t)rem, tile_base, src, dst, vsrc,
-                vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
+                vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
                 prof_t);
             prev_valid = (uint32_t)rem;
         }
