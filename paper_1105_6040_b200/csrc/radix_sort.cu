@@ -545,8 +545,10 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // per row against a warp-uniform running count (skewed passes), 5 the
     // early count's atomics return the in-warp ranks (lane-ordered, packed
     // 16-bit counters) and ranking is one lookup of the warp's digit base --
-    // for full TMA-landed tiles; other tiles rank as 1
-    constexpr bool ER = RANK == 5 && FULL && FROM_SMEM && !PIPE;
+    // for full TMA-landed tiles; other tiles rank as 1. 6 is 5 with 2's hot
+    // digit (ranked by ballots in the early phase), other tiles rank as 2.
+    constexpr bool ER = (RANK == 5 || RANK == 6) && FULL && FROM_SMEM && !PIPE;
+    constexpr int RB = RANK == 5 ? 1 : (RANK == 6 ? 2 : RANK);  // non-ER behaviour
     (void)prof_acc;
     (void)prof_t;
     (void)hot;
@@ -612,7 +614,51 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         for (int i = lane; i < kRadix / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
         __syncwarp();
     }
-    if constexpr (RANK == 2) {
+    if constexpr (ER) {
+        // in-warp ranks: item j of lane l precedes item j of lane l+1 and item
+        // j+1 of every lane, and same-word lanes of one atomic are served in
+        // lane order (b2s::probe_lane_order), so the old value is the rank.
+        // RANK 6: the hot digit's lanes take a warp-uniform running count
+        // plus their lanes below instead (same-address atomics serialise)
+        const uint32_t ecnt_a = smem_addr(ecnt);
+        const uint32_t lt = (1u << lane) - 1u;
+        uint32_t hot_run = 0;
+        constexpr int B = 4;
+#pragma unroll
+        for (int j0 = 0; j0 < ITEMS; j0 += B) {
+            uint32_t old[B], s16[B], hr[B];
+            bool h[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (j0 + b < ITEMS) {
+                    const uint32_t d = digit_of(keys[j0 + b], shift, dxor);
+                    s16[b] = 16 * (d & 1);
+                    if constexpr (RANK == 6) {
+                        h[b] = d == hot;
+                        const uint32_t hm = __ballot_sync(0xffffffffu, h[b]);
+                        hr[b] = hot_run + __popc(hm & lt);
+                        hot_run += __popc(hm);
+                        old[b] = atom_add_shared_if(!h[b], ecnt_a + 4 * (d >> 1), 1u << s16[b]);
+                    } else {
+                        old[b] = atom_add_shared(ecnt_a + 4 * (d >> 1), 1u << s16[b]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int j = j0 + b;
+                if (j < ITEMS) {
+                    uint32_t r = (old[b] >> s16[b]) & 0xFFFFu;
+                    if constexpr (RANK == 6) r = h[b] ? hr[b] : r;
+                    if (j & 1) rr[j >> 1] |= r << 16;
+                    else rr[j >> 1] = r;
+                }
+            }
+        }
+        if constexpr (RANK == 6) {
+            if (lane == 0 && hot_run) atomicAdd(ecnt + (hot >> 1), hot_run << (16 * (hot & 1)));
+        }
+    } else if constexpr (RB == 2) {
         uint32_t hot_n = 0;
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
@@ -623,33 +669,6 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             if (valid && !is_hot) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
         }
         if (lane == 0 && hot_n) atomicAdd(ecnt + ((hot & 1) * HALF + (hot >> 1)), hot_n);
-    } else if constexpr (ER) {
-        // in-warp ranks: item j of lane l precedes item j of lane l+1 and item
-        // j+1 of every lane, and same-word lanes of one atomic are served in
-        // lane order (b2s::probe_lane_order), so the old value is the rank
-        const uint32_t ecnt_a = smem_addr(ecnt);
-        constexpr int B = 4;
-#pragma unroll
-        for (int j0 = 0; j0 < ITEMS; j0 += B) {
-            uint32_t old[B], s16[B];
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                if (j0 + b < ITEMS) {
-                    const uint32_t d = digit_of(keys[j0 + b], shift, dxor);
-                    s16[b] = 16 * (d & 1);
-                    old[b] = atom_add_shared(ecnt_a + 4 * (d >> 1), 1u << s16[b]);
-                }
-            }
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const int j = j0 + b;
-                if (j < ITEMS) {
-                    const uint32_t r = (old[b] >> s16[b]) & 0xFFFFu;
-                    if (j & 1) rr[j >> 1] |= r << 16;
-                    else rr[j >> 1] = r;
-                }
-            }
-        }
     } else {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
@@ -752,7 +771,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             sts_key(keys_a + swz<sizeof(U), SWZ>(r) * (uint32_t)sizeof(U), keys[j]);
             if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(r), vals[j]);
         }
-    } else if constexpr (RANK == 2 && FULL) {
+    } else if constexpr (RB == 2 && FULL) {
         // hot lanes: the warp's running offset of the hot digit (nobody
         // else touches its counter) plus the lanes below in this row
         uint32_t hot_run = (s_cnt[warp * HALF + (hot >> 1)] >> (16 * (hot & 1))) & 0xFFFFu;
@@ -782,7 +801,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                 }
             }
         }
-    } else if constexpr ((RANK == 1 || RANK == 5) && FULL) {
+    } else if constexpr (RB == 1 && FULL) {
         // atomic ranking in batches of 4 items: the batch's atomics are
         // independent (the warp's shared accesses stay in program order, so
         // the counters advance exactly as item by item) and their latencies
@@ -817,7 +836,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         const uint32_t peers = 1u << lane;
 #else
         uint32_t r;
-        if constexpr (RANK >= 1) {
+        if constexpr (RB >= 1) {
             // lane-ordered shared atomics: lanes adding to the same counter in one
             // warp instruction receive old values in ascending lane order on this
             // device (verified at context creation by b2s::probe_lane_order), so
@@ -940,7 +959,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #pragma unroll
         for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
     }
-    writeout_tile<U, VALS, LB, THREADS, ITEMS, RANK == 2, SWZ>(sbuf, svbuf, gbase_out, tile_valid, dst,
+    writeout_tile<U, VALS, LB, THREADS, ITEMS, RB == 2, SWZ>(sbuf, svbuf, gbase_out, tile_valid, dst,
                                                                vdst, shift, dxor, nd);
 }
 
@@ -970,7 +989,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     // take the SMs as the predecessor's drain, and the ones not suited to the
     // pass exit at once. What they decide on (the pass's histogram, the
     // prologue's order statistic) was final before 2 started.
-    constexpr int TR = RANK == 3 ? 2 : (RANK >= 1 ? (B2S_ERANK ? 5 : 1) : 0);
+    constexpr int TR = RANK == 3 ? (B2S_ERANK ? 6 : 2) : (RANK >= 1 ? (B2S_ERANK ? 5 : 1) : 0);
     // separate landing / staging buffers: measured per 2^28-key u32 pass,
     // uniform keys 0.776 ms in place vs 0.794 separate, ascending (the
     // structured twin) 0.709 vs 0.699 -- so only the structured twin uses it
