@@ -71,6 +71,7 @@ struct RadixPlan {
     int do_copy;
     int need_fallback;  // first active digit is not digit 0: recount it
     int structured;     // input nearly sorted either way: swizzled staging
+    int all_hist;       // every digit's histogram came from the prologue (no in-pass counting)
     int digit[kMaxSlots];
     uint32_t dxor[kMaxSlots];  // 0x80 on the top digit of signed keys
     const unsigned long long* hist[kMaxSlots];  // digit histogram per slot
@@ -89,6 +90,7 @@ struct RadixPlan {
 struct RadixCounters {
     unsigned long long hist[kMaxSlots][256];  // slot s's digit histogram
     unsigned long long spec0[256];            // prologue's digit-0 histogram
+    unsigned long long dhist[4][256];         // 4-byte keys: every digit's histogram (prologue)
     unsigned long long or_all;                // OR of all keys
     unsigned long long nor_all;               // OR of all complemented keys
     unsigned long long asc_pairs, desc_pairs;  // sampled adjacent pairs in order / reversed

@@ -228,3 +228,38 @@ def test_n_at_least_2p30_uses_64bit_lookback(ctx):
     assert inv == 0 and ms_in == ms_out
     del keys, out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint32])
+@pytest.mark.parametrize("kind", ["uniform", "skewed", "lowzero", "midconst", "topbyte", "sorted",
+                                  "extremes", "equal"])
+def test_all_digit_prologue_sizes(ctx, dt, kind):
+    """4-byte keys from 2^22 keys up take every digit histogram from the
+    all-digit prologue (signed top digit counted with its sign flip, constant
+    digits skipped, no in-pass counting): bit-exact against numpy."""
+    rng = np.random.default_rng(11)
+    for n in ((1 << 22) - 1, 1 << 22, (1 << 22) + 12345):
+        keys = rand_keys(n, dt, rng, kind)
+        out, _ = ctx.sort(to_dev(keys))
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(out, dt), np.sort(keys)), (kind, n)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint32])
+def test_all_digit_prologue_pairs_and_unaligned(ctx, dt):
+    rng = np.random.default_rng(12)
+    n = (1 << 22) + 77
+    keys = rand_keys(n, dt, rng, "dups")
+    vals = np.arange(n, dtype=np.uint32)
+    dv = torch.from_numpy(vals.view(np.int32)).cuda().view(torch.uint32)
+    out, vout = ctx.sort(to_dev(keys), vals=dv)
+    torch.cuda.synchronize()
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(to_host(out, dt), keys[order])
+    assert np.array_equal(vout.view(torch.int32).cpu().numpy().view(np.uint32), order.astype(np.uint32))
+    # input one element past a 16-byte boundary: scalar prologue loads, no TMA
+    keys = rand_keys(n + 1, dt, rng)
+    d = to_dev(keys)[1:]
+    out, _ = ctx.sort(d)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(out, dt), np.sort(keys[1:]))

@@ -1,6 +1,6 @@
 """A/B timing of onesweep development builds (u32 keys only).
 
-  python tools/kdev.py lib1.so [lib2.so ...]      (on the GPU box)
+  python tools/kdev.py lib1.so [VAR=1,lib2.so ...]      (on the GPU box)
 
 Each library runs in its own process (B2S_LIB): uniform, Zipf-like and
 ascending 2^28 u32 sorts, checked against torch.sort, reporting the average
@@ -46,12 +46,16 @@ print(" | ".join(res))
 
 
 def main():
-    for lib in sys.argv[1:]:
+    for arg in sys.argv[1:]:
         env = dict(os.environ)
+        *sets, lib = arg.split(",")  # optional VAR=VALUE settings before the library
+        for kv in sets:
+            k, v = kv.split("=", 1)
+            env[k] = v
         env["B2S_LIB"] = os.path.abspath(lib)
         r = subprocess.run([sys.executable, "-c", CODE % ROOT], env=env, capture_output=True, text=True)
         tail = r.stdout.strip() or r.stderr.strip()[-400:]
-        print(f"{os.path.basename(lib):28s} {tail}", flush=True)
+        print(f"{','.join(sets + [os.path.basename(lib)]):40s} {tail}", flush=True)
 
 
 if __name__ == "__main__":
