@@ -425,6 +425,9 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_SEP
 #define B2S_SEP 1
 #endif
+#ifndef B2S_EARLY_LB
+#define B2S_EARLY_LB 0
+#endif
 #ifndef B2S_ERANK_RELOAD
 #define B2S_ERANK_RELOAD 1
 #endif
@@ -663,6 +666,11 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // digit (ranked by ballots in the early phase), other tiles rank as 2.
     constexpr bool ER = (RANK == 5 || RANK == 6) && FULL && FROM_SMEM && !PIPE;
     constexpr int RB = RANK == 5 ? 1 : (RANK == 6 ? 2 : RANK);  // non-ER behaviour
+    // ELB (experiment, off): the look-back runs right after the digit section
+    // (its warps rank afterwards), so inclusive prefixes are published
+    // earlier. Measured per 2^28-key u32 pass: 0.726 ms off, 0.86 on, 0.81 on
+    // with separate staging -- the ranking hides the look-back's latency
+    constexpr bool ELB = ER && B2S_EARLY_LB;
     (void)prof_acc;
     (void)prof_t;
     (void)hot;
@@ -852,6 +860,70 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         for (int w = 0; w < WARPS; ++w) s_cnt[w * HALF + tid] += add;
     }
     __syncthreads();
+    // ---- decoupled look-back: one lane per digit. The first PRE predecessors
+    // were fetched before ranking; later steps read LOOKBACK at a time
+    // (independent loads) in a warp-uniform loop. Each lane publishes its
+    // inclusive prefix the moment it is known.
+    auto lookback = [&]() {
+        if (tid < kRadix) {
+            unsigned long long excl = 0;
+            const uint32_t mycount = (tid + 1 < kRadix ? sh.start[tid + 1] : (uint32_t)tile_valid) - sh.start[tid];
+    #ifdef B2S_ABLATE_LOOKBACK
+            if (false) {
+    #else
+            if (tile > 0) {
+    #endif
+                int64_t pred = (int64_t)tile - 1;
+                bool done = false;
+                const LB* col = lb_cur + tid;
+                LB* mine = lb_cur + (size_t)tile * kRadix + tid;
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                bool stop = false;
+    #pragma unroll
+                for (int i = 0; i < PRE; ++i) {
+                    if (!stop) {
+                        const LB w = ((int64_t)tile - 1 - i >= 0) ? sh.lbw[i * kRadix + tid] : W::kInc;
+                        const LB f = W::flag(w);
+                        if (f != 0) {
+                            excl += (unsigned long long)(w & W::kMask);
+                            done = (f == 2);
+                            stop = done;
+                            pred -= done ? 0 : 1;
+                        } else {
+                            stop = true;
+                        }
+                    }
+                }
+                if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
+                while (__any_sync(0xffffffffu, !done)) {
+    #ifdef B2S_PHASE_PROFILE
+                    if (tid == 0) prof_acc[7] += 1;
+    #endif
+                    if (!done) {
+                        LB w[LOOKBACK];
+    #pragma unroll
+                        for (int i = 0; i < LOOKBACK; ++i)
+                            w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * kRadix) : W::kInc;
+                        stop = false;
+    #pragma unroll
+                        for (int i = 0; i < LOOKBACK; ++i) {
+                            const LB f = W::flag(w[i]);
+                            if (!stop && f != 0) {
+                                excl += (unsigned long long)(w[i] & W::kMask);
+                                done = (f == 2);
+                                stop = done;
+                                pred -= done ? 0 : 1;
+                            } else {
+                                stop = true;
+                            }
+                        }
+                        if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
+                    }
+                }
+            }
+            gbase_out[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
+        }
+    };
 #if B2S_ERANK_RELOAD
     if constexpr (ER) {
         // only the packed ranks were held across the digit section; the keys
@@ -866,6 +938,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         if constexpr (!SEP) __syncthreads();  // in-place staging: all reads first
     }
 #endif
+    if constexpr (ELB) lookback();
     B2S_PHASE(2);
 
     // ---- rank within the tile and stage digit-sorted in shared memory. The
@@ -1000,68 +1073,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         between();
     }
 
-    // ---- decoupled look-back: one lane per digit. The first PRE predecessors
-    // were fetched before ranking; later steps read LOOKBACK at a time
-    // (independent loads) in a warp-uniform loop. Each lane publishes its
-    // inclusive prefix the moment it is known.
-    if (tid < kRadix) {
-        unsigned long long excl = 0;
-        const uint32_t mycount = (tid + 1 < kRadix ? sh.start[tid + 1] : (uint32_t)tile_valid) - sh.start[tid];
-#ifdef B2S_ABLATE_LOOKBACK
-        if (false) {
-#else
-        if (tile > 0) {
-#endif
-            int64_t pred = (int64_t)tile - 1;
-            bool done = false;
-            const LB* col = lb_cur + tid;
-            LB* mine = lb_cur + (size_t)tile * kRadix + tid;
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            bool stop = false;
-#pragma unroll
-            for (int i = 0; i < PRE; ++i) {
-                if (!stop) {
-                    const LB w = ((int64_t)tile - 1 - i >= 0) ? sh.lbw[i * kRadix + tid] : W::kInc;
-                    const LB f = W::flag(w);
-                    if (f != 0) {
-                        excl += (unsigned long long)(w & W::kMask);
-                        done = (f == 2);
-                        stop = done;
-                        pred -= done ? 0 : 1;
-                    } else {
-                        stop = true;
-                    }
-                }
-            }
-            if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
-            while (__any_sync(0xffffffffu, !done)) {
-#ifdef B2S_PHASE_PROFILE
-                if (tid == 0) prof_acc[7] += 1;
-#endif
-                if (!done) {
-                    LB w[LOOKBACK];
-#pragma unroll
-                    for (int i = 0; i < LOOKBACK; ++i)
-                        w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * kRadix) : W::kInc;
-                    stop = false;
-#pragma unroll
-                    for (int i = 0; i < LOOKBACK; ++i) {
-                        const LB f = W::flag(w[i]);
-                        if (!stop && f != 0) {
-                            excl += (unsigned long long)(w[i] & W::kMask);
-                            done = (f == 2);
-                            stop = done;
-                            pred -= done ? 0 : 1;
-                        } else {
-                            stop = true;
-                        }
-                    }
-                    if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
-                }
-            }
-        }
-        gbase_out[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
-    }
+    if constexpr (!ELB) lookback();
     if constexpr (PIPE) return;  // the caller syncs; this tile is written next round
     __syncthreads();
     B2S_PHASE(4);
@@ -1107,7 +1119,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     // separate landing / staging buffers: measured per 2^28-key u32 pass,
     // uniform keys 0.776 ms in place vs 0.794 separate, ascending (the
     // structured twin) 0.709 vs 0.699 -- so only the structured twin uses it
-    constexpr bool SEP = TR == 5 && RANK == 4 && B2S_SEP;
+    constexpr bool SEP = TR == 5 && (RANK == 4 || B2S_SEP > 1) && B2S_SEP;
     constexpr bool SWZ = RANK == 4;
     if constexpr (RANK == 2 || RANK == 3)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
