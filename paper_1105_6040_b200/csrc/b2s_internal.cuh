@@ -90,7 +90,7 @@ struct RadixPlan {
 struct RadixCounters {
     unsigned long long hist[kMaxSlots][256];  // slot s's digit histogram
     unsigned long long spec0[256];            // prologue's digit-0 histogram
-    unsigned long long dhist[4][256];         // 4-byte keys: every digit's histogram (prologue)
+    unsigned long long dhist[8][256];         // every digit's histogram (all-digit prologue)
     unsigned long long or_all;                // OR of all keys
     unsigned long long nor_all;               // OR of all complemented keys
     unsigned long long asc_pairs, desc_pairs;  // sampled adjacent pairs in order / reversed

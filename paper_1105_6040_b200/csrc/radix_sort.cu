@@ -215,78 +215,100 @@ __global__ void __launch_bounds__(512, kPrologueMinBlocks<U>) radix_prologue_ker
     }
 }
 
-// All-digit prologue for 4-byte keys: the four digit histograms in one read,
-// so the passes need not count the next digit on their way out (that count
-// is a random shared atomic per key, ~7% of a pass). Each lane owns a column
-// of counters (s_hl[digit][bin][lane]: the bank is the lane), so the four
-// per-key shared reductions are conflict-free; one CTA of 1024 threads per
-// SM holds the 128 KB of columns. Also the OR / OR-of-complement and the
+// All-digit prologue: every digit histogram in one read, so the passes need
+// not count the next digit on their way out (that count is a random shared
+// atomic per key, ~7% of a pass). Lanes own columns of counters
+// (s_hl[digit][bin][column]): 4-byte keys give each lane its own column (the
+// bank is the lane: the four per-key shared reductions are conflict-free);
+// 8-byte keys have 8 digits, so lanes l and l+16 share one of 16 columns
+// (at most 2-way conflicts) and the columns still fit 128 KB. One
+// 1024-thread CTA per SM. Also the OR / OR-of-complement and the
 // adjacent-pair order sample of the regular prologue.
+#ifndef B2S_ALLHIST_DEPTH
+#define B2S_ALLHIST_DEPTH 8  // 8: 0.227 -> 0.217 ms for 2^28 u32 (4)
+#endif
 constexpr int kAllHistThreads = 1024;
-constexpr size_t kAllHistSmem = 4 * 256 * 32 * 4;
+constexpr size_t kAllHistSmem = 128 * 1024;
 constexpr uint64_t kAllHistMinKeys = 1ull << 22;
 
+template <typename U>
 __global__ void __launch_bounds__(kAllHistThreads, 1)
-    radix_prologue_all_kernel(const uint32_t* __restrict__ keys, uint64_t n,
+    radix_prologue_all_kernel(const U* __restrict__ keys, uint64_t n,
                               RadixCounters* __restrict__ ctr, uint4* __restrict__ lb_zero,
                               uint64_t lb_zero_vecs, uint32_t top_xor) {
-    extern __shared__ __align__(16) uint32_t s_hl[];  // [4][256][32]
+    constexpr int ND = sizeof(U);            // digits
+    constexpr int COLS = sizeof(U) == 4 ? 32 : 16;
+    constexpr int VEC = 16 / sizeof(U);      // keys per 16-byte load
+    static_assert((size_t)ND * 256 * COLS * 4 == kAllHistSmem, "column layout");
+    extern __shared__ __align__(16) uint32_t s_hl[];  // [ND][256][COLS]
     __shared__ unsigned long long s_or[32], s_nor[32];
     __shared__ uint2 s_ord[32];
     for (int i = threadIdx.x; i < (int)(kAllHistSmem / 16); i += blockDim.x)
         reinterpret_cast<uint4*>(s_hl)[i] = make_uint4(0, 0, 0, 0);
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t hb = (uint32_t)__cvta_generic_to_shared(s_hl) + 4u * lane;
-    const uint32_t tx7 = top_xor << 7;
+    const uint32_t hb = (uint32_t)__cvta_generic_to_shared(s_hl) + 4u * (lane & (COLS - 1));
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = tid; i < lb_zero_vecs; i += stride) lb_zero[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     unsigned long long o = 0, no = 0;
     uint32_t asc = 0, desc = 0;
-    // counter address of (digit p, bin b) in this lane's column: hb + p*32 KB + b*128
-    auto count = [&](uint32_t e) {
-        o |= e;
-        no |= (uint32_t)~e;
-        const uint32_t a0 = (e << 7) & 0x7F80u;
-        const uint32_t a1 = (e >> 1) & 0x7F80u;
-        const uint32_t a2 = (e >> 9) & 0x7F80u;
-        const uint32_t a3 = ((e >> 17) & 0x7F80u) ^ tx7;
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hb + a0) : "memory");
-        asm volatile("red.shared.add.u32 [%0+32768], 1;" ::"r"(hb + a1) : "memory");
-        asm volatile("red.shared.add.u32 [%0+65536], 1;" ::"r"(hb + a2) : "memory");
-        asm volatile("red.shared.add.u32 [%0+98304], 1;" ::"r"(hb + a3) : "memory");
+    // counter of (digit p, bin b) in this lane's column: hb + (p*256 + b)*COLS*4
+    auto count = [&](U e) {
+        o |= (unsigned long long)e;
+        no |= (unsigned long long)(U)~e;
+        if constexpr (sizeof(U) == 4) {
+            const uint32_t tx7 = top_xor << 7;
+            const uint32_t a0 = ((uint32_t)e << 7) & 0x7F80u;
+            const uint32_t a1 = ((uint32_t)e >> 1) & 0x7F80u;
+            const uint32_t a2 = ((uint32_t)e >> 9) & 0x7F80u;
+            const uint32_t a3 = (((uint32_t)e >> 17) & 0x7F80u) ^ tx7;
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hb + a0) : "memory");
+            asm volatile("red.shared.add.u32 [%0+32768], 1;" ::"r"(hb + a1) : "memory");
+            asm volatile("red.shared.add.u32 [%0+65536], 1;" ::"r"(hb + a2) : "memory");
+            asm volatile("red.shared.add.u32 [%0+98304], 1;" ::"r"(hb + a3) : "memory");
+        } else {
+            const uint32_t lo = (uint32_t)e, hi = (uint32_t)((unsigned long long)e >> 32);
+            const uint32_t tx6 = top_xor << 6;
+            // bin * 64 bytes: byte k of a word at bits 6..13
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hb + ((lo << 6) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+16384], 1;" ::"r"(hb + ((lo >> 2) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+32768], 1;" ::"r"(hb + ((lo >> 10) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+49152], 1;" ::"r"(hb + ((lo >> 18) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+65536], 1;" ::"r"(hb + ((hi << 6) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+81920], 1;" ::"r"(hb + ((hi >> 2) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+98304], 1;" ::"r"(hb + ((hi >> 10) & 0x3FC0u)) : "memory");
+            asm volatile("red.shared.add.u32 [%0+114688], 1;" ::"r"(hb + (((hi >> 18) & 0x3FC0u) ^ tx6))
+                         : "memory");
+        }
     };
     const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
     uint64_t head = 0;
     if (aligned) {
         const uint4* kv = reinterpret_cast<const uint4*>(keys);
-        const uint64_t nvec = n / 4;
+        const uint64_t nvec = n / VEC;
         uint64_t v = tid;
-        for (; v + 3 * stride < nvec; v += 4 * stride) {  // 4 independent 16-B loads in flight
-            uint4 q[4];
+        constexpr int QD = B2S_ALLHIST_DEPTH;  // independent 16-B loads in flight per thread
+        for (; v + (QD - 1) * stride < nvec; v += QD * stride) {
+            uint4 q[QD];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) q[u] = __ldcs(kv + v + u * stride);
+            for (int u = 0; u < QD; ++u) q[u] = __ldcs(kv + v + u * stride);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                count(q[u].x);
-                count(q[u].y);
-                count(q[u].z);
-                count(q[u].w);
+            for (int u = 0; u < QD; ++u) {
+                const U(&e)[VEC] = *reinterpret_cast<const U(*)[VEC]>(&q[u]);
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) count(e[j]);
             }
-            const uint32_t e[4] = {q[0].x, q[0].y, q[0].z, q[0].w};
-            order_pairs<uint32_t, 4>(e, asc, desc);
+            order_pairs<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q[0]), asc, desc);
         }
         for (; v < nvec; v += stride) {
             const uint4 q = __ldcs(kv + v);
-            count(q.x);
-            count(q.y);
-            count(q.z);
-            count(q.w);
-            const uint32_t e[4] = {q.x, q.y, q.z, q.w};
-            order_pairs<uint32_t, 4>(e, asc, desc);
+            const U(&e)[VEC] = *reinterpret_cast<const U(*)[VEC]>(&q);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) count(e[j]);
+            order_pairs<U, VEC>(e, asc, desc);
         }
-        head = nvec * 4;
+        head = nvec * VEC;
     }
     for (uint64_t i = head + tid; i < n; i += stride) count(keys[i]);
 #pragma unroll
@@ -318,12 +340,12 @@ __global__ void __launch_bounds__(kAllHistThreads, 1)
         if (a) atomicAdd(&ctr->asc_pairs, a);
         if (d) atomicAdd(&ctr->desc_pairs, d);
     }
-    // column sums: thread i sums row i starting at lane i (conflict-free)
-    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
-        const uint32_t* row = s_hl + i * 32;
+    // column sums: thread i sums row i starting at column i (spread banks)
+    for (int i = threadIdx.x; i < ND * 256; i += blockDim.x) {
+        const uint32_t* row = s_hl + i * COLS;
         uint32_t sum = 0;
 #pragma unroll 8
-        for (int l = 0; l < 32; ++l) sum += row[(l + i) & 31];
+        for (int l = 0; l < COLS; ++l) sum += row[(l + i) & (COLS - 1)];
         if (sum) atomicAdd(&ctr->dhist[i >> 8][i & 255], (unsigned long long)sum);
     }
 }
@@ -1861,14 +1883,15 @@ struct TileCfg {
     int threads, items;
 };
 
-// B2S_ALL_HIST=0 counts each next digit inside the passes instead
-bool all_hist_enabled() {
+// B2S_ALL_HIST: 1 (default) all-digit prologue for 4-byte keys, 2 also for
+// 8-byte keys, 0 never (each next digit is counted inside the passes)
+int all_hist_mode() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("B2S_ALL_HIST");
         v = e ? atoi(e) : 1;
     }
-    return v != 0;
+    return v;
 }
 
 int onesweep_cfg() {
@@ -2090,19 +2113,22 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     const bool wide = n >= (1ull << 30);
     ctx->ev_hist0 = record(ctx);
     B2S_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RadixCounters), ctx->stream));
-    // 4-byte keys past a few million: every digit histogram up front
-    const bool all_hist = sizeof(U) == 4 && n >= kAllHistMinKeys && all_hist_enabled();
+    // 4-byte keys past a few million: every digit histogram up front. 8-byte
+    // keys only with B2S_ALL_HIST=2: measured for 2^28 u64 + u32 payload, the
+    // 8-digit prologue takes 0.57 ms vs 0.37 for the digit-0 one, and the
+    // pairs' passes gain nothing from skipping the in-pass count (1.96 ms)
+    const bool all_hist = n >= kAllHistMinKeys && all_hist_mode() >= (sizeof(U) == 4 ? 1 : 2);
     if (all_hist) {
         static bool attr = false;
         if (!attr) {
-            B2S_CUDA(cudaFuncSetAttribute(radix_prologue_all_kernel,
+            B2S_CUDA(cudaFuncSetAttribute(radix_prologue_all_kernel<U>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAllHistSmem));
             attr = true;
         }
-        const uint64_t want = (n / 4 + kAllHistThreads * 4 - 1) / (kAllHistThreads * 4);
+        const uint64_t want = (n / (16 / sizeof(U)) + kAllHistThreads * 4 - 1) / (kAllHistThreads * 4);
         const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)ctx->num_sms);
-        radix_prologue_all_kernel<<<grid, kAllHistThreads, kAllHistSmem, ctx->stream>>>(
-            static_cast<const uint32_t*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
+        radix_prologue_all_kernel<U><<<grid, kAllHistThreads, kAllHistSmem, ctx->stream>>>(
+            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
             (lb_region + 15) / 16, top_xor);
         B2S_LAUNCHED();
     } else {
@@ -2118,7 +2144,7 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     radix_plan_kernel<<<1, 32, 0, ctx->stream>>>(plan, ctr, NP, n, top_xor, kin, kout,
                                                  sc->alt_keys, vin, vout, sc->alt_vals, all_hist ? 1 : 0);
     B2S_LAUNCHED();
-    if (n > 0) {
+    if (n > 0 && !all_hist) {  // the all-digit prologue needs no recount
         int grid = (int)std::min<uint64_t>((n + 511) / 512, (uint64_t)ctx->num_sms * 4);
         radix_fallback_hist_kernel<U><<<grid, 512, 0, ctx->stream>>>(plan, static_cast<const U*>(kin),
                                                                      n, ctr);

@@ -230,13 +230,15 @@ def test_n_at_least_2p30_uses_64bit_lookback(ctx):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("dt", [np.int32, np.uint32])
+@pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("kind", ["uniform", "skewed", "lowzero", "midconst", "topbyte", "sorted",
                                   "extremes", "equal"])
 def test_all_digit_prologue_sizes(ctx, dt, kind):
-    """4-byte keys from 2^22 keys up take every digit histogram from the
+    """From 2^22 keys up, 4-byte keys take every digit histogram from the
     all-digit prologue (signed top digit counted with its sign flip, constant
-    digits skipped, no in-pass counting): bit-exact against numpy."""
+    digits skipped, no in-pass counting); 8-byte keys the digit-0 prologue
+    and in-pass counts (tests/test_gpu_rank_modes.py runs them through the
+    8-digit prologue too): bit-exact against numpy."""
     rng = np.random.default_rng(11)
     for n in ((1 << 22) - 1, 1 << 22, (1 << 22) + 12345):
         keys = rand_keys(n, dt, rng, kind)
@@ -245,7 +247,7 @@ def test_all_digit_prologue_sizes(ctx, dt, kind):
         assert np.array_equal(to_host(out, dt), np.sort(keys)), (kind, n)
 
 
-@pytest.mark.parametrize("dt", [np.int32, np.uint32])
+@pytest.mark.parametrize("dt", DTYPES)
 def test_all_digit_prologue_pairs_and_unaligned(ctx, dt):
     rng = np.random.default_rng(12)
     n = (1 << 22) + 77
