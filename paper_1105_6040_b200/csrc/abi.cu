@@ -368,26 +368,30 @@ b2s_status b2s_sort_batch(b2s_ctx* ctx, b2s_dtype dtype, const void* const* keys
     if (count == 0 || n == 0) return B2S_OK;
     const bool with_vals = vals_in != nullptr;
     const size_t kb = (size_t)key_bytes(dtype) * n, vb = 4 * n;
-    // two device stages; stage b holds array i (i % 2 == b) from its upload
-    // to the end of its download
-    B2S_TRY(ctx->stage_in.ensure(2 * kb));
-    if (with_vals) B2S_TRY(ctx->stage_vin.ensure(2 * vb));
+    // three device stages; stage b holds array i (i % 3 == b) from its upload
+    // to the end of its download, so upload i+1, sort i and download i-1 run
+    // at once and both PCIe directions stay busy (with two stages the upload
+    // of i+2 waits for the download of i, which waits for the sort of i: the
+    // upload stream idled for one sort per array)
+    constexpr int NS = 3;
+    B2S_TRY(ctx->stage_in.ensure(NS * kb));
+    if (with_vals) B2S_TRY(ctx->stage_vin.ensure(NS * vb));
     cudaStream_t comp = ctx->stream;
     cudaStream_t up = nullptr, down = nullptr;
-    cudaEvent_t ev_up[2] = {}, ev_sorted[2] = {}, ev_down[2] = {};
+    cudaEvent_t ev_up[NS] = {}, ev_sorted[NS] = {}, ev_down[NS] = {};
     b2s_status st = B2S_OK;
     cudaError_t e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking);
-    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    for (int b = 0; b < NS && e == cudaSuccess; ++b) {
         e = cudaEventCreateWithFlags(&ev_up[b], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_sorted[b], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_down[b], cudaEventDisableTiming);
     }
     for (int i = 0; i < count && e == cudaSuccess && st == B2S_OK; ++i) {
-        const int b = i & 1;
+        const int b = i % NS;
         char* dk = static_cast<char*>(ctx->stage_in.ptr) + b * kb;
         uint32_t* dv = with_vals ? static_cast<uint32_t*>(ctx->stage_vin.ptr) + b * n : nullptr;
-        if (i >= 2) e = cudaStreamWaitEvent(up, ev_down[b], 0);  // stage b downloaded
+        if (i >= NS) e = cudaStreamWaitEvent(up, ev_down[b], 0);  // stage b downloaded
         if (e == cudaSuccess) e = cudaMemcpyAsync(dk, keys_in[i], kb, cudaMemcpyHostToDevice, up);
         if (e == cudaSuccess && with_vals)
             e = cudaMemcpyAsync(dv, vals_in[i], vb, cudaMemcpyHostToDevice, up);
@@ -408,7 +412,7 @@ b2s_status b2s_sort_batch(b2s_ctx* ctx, b2s_dtype dtype, const void* const* keys
     if (down) cudaStreamSynchronize(down);
     if (up) cudaStreamSynchronize(up);
     cudaStreamSynchronize(comp);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
         if (ev_up[b]) cudaEventDestroy(ev_up[b]);
         if (ev_sorted[b]) cudaEventDestroy(ev_sorted[b]);
         if (ev_down[b]) cudaEventDestroy(ev_down[b]);
