@@ -1002,7 +1002,17 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         const uint32_t* wc = s_cnt + warp * HALF;
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
+#if B2S_ERANK_RELOAD
             const uint32_t d = digit_of(keys[j], shift, dxor);
+#else
+            // recomputed behind an opaque op: keeping the early phase's digits
+            // live across the digit section would cost ITEMS more registers
+            uint32_t w, d;
+            if constexpr (sizeof(U) == 4) w = (uint32_t)keys[j];
+            else w = shift >= 32 ? (uint32_t)((unsigned long long)keys[j] >> 32) : (uint32_t)keys[j];
+            asm volatile("prmt.b32 %0, %1, 0, %2;" : "=r"(d) : "r"(w), "r"(0x4440u | ((shift >> 3) & 3)));
+            d ^= dxor;
+#endif
             const uint32_t r = ((wc[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) + ((rr[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
             sts_key(keys_a + swz<sizeof(U), SWZ>(r) * (uint32_t)sizeof(U), keys[j]);
             if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(r), vals[j]);
