@@ -78,10 +78,46 @@ struct MergeItems {
 #endif
 };
 
+// 16 bytes global -> shared, asynchronously (both addresses 16-byte aligned)
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+// Element phase of a global address within its 16-byte word.
+template <typename T>
+__device__ __forceinline__ uint32_t phase16(const T* p) {
+    return (uint32_t)((reinterpret_cast<uintptr_t>(p) & 15u) / sizeof(T));
+}
+
+// Copies n elements src[0..n) to sdst[0..n) where sdst's address has the same
+// 16-byte phase as src's: 16-byte cp.async for the aligned middle, single
+// elements for the head and tail. All threads of the CTA take part.
+template <typename T>
+__device__ __forceinline__ void stage_slice(T* sdst, const T* src, uint32_t n) {
+    constexpr uint32_t V = 16 / sizeof(T);
+    const uint32_t ph = phase16(src);
+    const uint32_t head = std::min<uint32_t>((V - ph) % V, n);
+    const uint32_t nv = (n - head) / V;
+    const uint32_t tail0 = head + nv * V;
+    for (uint32_t v = threadIdx.x; v < nv; v += kMergeThreads)
+        cp_async_16(sdst + head + v * V, src + head + v * V);
+    const uint32_t t = threadIdx.x;
+    if (t < head) cp_async_elem(sdst + t, src + t);
+    else if (t >= V && t - V < n - tail0) cp_async_elem(sdst + tail0 + (t - V), src + tail0 + (t - V));
+}
+
 // Merges output positions [out_lo, out_hi) of merge(A, B) into out[0 ..).
 // Used both for full merges (out_lo = 0) and for merge_split's kept half.
-// (A persistent variant that streams tile t + gridDim.x into a second buffer
-// while tile t merges measured slower: 2.21 vs 1.78 ms for 8 runs of 2^25.)
+// The A and B slices are staged in shared memory at the same 16-byte phase as
+// in global memory (vector copies), merged (heads in registers), restaged at
+// the output's phase and written with 16-byte stores. (A persistent variant
+// that streams tile t + gridDim.x into a second buffer while tile t merges
+// measured slower: 2.21 vs 1.78 ms for 8 runs of 2^25.)
+// Measured per 2-way round of 2^28 i32 keys: element-wise staging and stores
+// 0.553 ms (53 instructions per output), vectorised 0.539 ms (48); the round
+// is bound by shared-memory wavefronts (L1 79% busy: the merge loop's one
+// load per output hits lanes' scattered heads) and issue (73%).
 template <typename T, bool VALS>
 __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     const T* __restrict__ a, const uint32_t* __restrict__ va, uint64_t na,
@@ -90,8 +126,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     uint32_t* __restrict__ vout) {
     constexpr int ITEMS = MergeItems<T>::value;
     constexpr int TILE = kMergeThreads * ITEMS;
-    __shared__ T s_k[TILE + 1];  // +1: the merge loop may read one past the end
-    __shared__ uint32_t s_v[VALS ? TILE : 1];
+    constexpr uint32_t V = 16 / sizeof(T);
+    __shared__ __align__(16) T s_k[TILE + 3 * V + 1];  // two phase-aligned slices (+1: one read past the end)
+    __shared__ __align__(16) uint32_t s_v[VALS ? TILE + 3 * 4 + 1 : 1];
 
     const uint64_t t = blockIdx.x;
     const uint64_t d0 = out_lo + t * TILE;
@@ -100,51 +137,83 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     const uint64_t b0 = d0 - a0;
     const uint32_t la = (uint32_t)(a1 - a0), cnt = (uint32_t)(d1 - d0), lb = cnt - la;
 
-    // stage A's slice then B's with asynchronous copies (no registers held,
-    // every copy of the tile in flight at once)
-    for (uint32_t i = threadIdx.x; i < cnt; i += kMergeThreads) {
-        cp_async_elem(&s_k[i], i < la ? a + a0 + i : b + b0 + (i - la));
-        if constexpr (VALS) cp_async_elem(&s_v[i], i < la ? va + a0 + i : vb + b0 + (i - la));
+    // A at s_k[pa ..), B at s_k[sb ..): each at its global 16-byte phase
+    const uint32_t pa = phase16(a + a0);
+    const uint32_t sb = (pa + la + V - 1) / V * V + phase16(b + b0);
+    T* sa_ = s_k + pa;
+    T* sb_ = s_k + sb;
+    stage_slice(sa_, a + a0, la);
+    stage_slice(sb_, b + b0, lb);
+    uint32_t* sva = nullptr;
+    uint32_t* svb = nullptr;
+    if constexpr (VALS) {
+        const uint32_t qa = phase16(va + a0);
+        const uint32_t qb = (qa + la + 3) / 4 * 4 + phase16(vb + b0);
+        sva = s_v + qa;
+        svb = s_v + qb;
+        stage_slice(sva, va + a0, la);
+        stage_slice(svb, vb + b0, lb);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
 
     const uint32_t diag = std::min<uint32_t>(threadIdx.x * ITEMS, cnt);
-    uint32_t ai = merge_path_smem(s_k, la, s_k + la, lb, diag);
-    uint32_t bi = la + diag - ai;  // index into the staged B
+    uint32_t ai = merge_path_smem(sa_, la, sb_, lb, diag);
+    uint32_t bi = diag - ai;
     // the two heads live in registers: one shared load per output
-    T ka = s_k[ai], kb = s_k[bi];
+    T ka = sa_[ai], kb = sb_[bi];
     T rk[ITEMS];
     uint32_t rv[VALS ? ITEMS : 1];
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         if (diag + j < cnt) {
-            const bool take_a = bi >= cnt || (ai < la && !(kb < ka));
+            const bool take_a = bi >= lb || (ai < la && !(kb < ka));
             rk[j] = take_a ? ka : kb;
-            if constexpr (VALS) rv[j] = s_v[take_a ? ai : bi];
-            const uint32_t nxt = take_a ? ++ai : ++bi;
-            const T kn = s_k[nxt];
-            if (take_a) ka = kn;
-            else kb = kn;
+            if constexpr (VALS) rv[j] = take_a ? sva[ai] : svb[bi];
+            if (take_a) ka = sa_[++ai];
+            else kb = sb_[++bi];
         }
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        if (diag + j < cnt) {
-            s_k[threadIdx.x * ITEMS + j] = rk[j];
-            if constexpr (VALS) s_v[threadIdx.x * ITEMS + j] = rv[j];
-        }
-    }
-    __syncthreads();
+    // restage at the output's 16-byte phase, then 16-byte stores
     const uint64_t o = d0 - out_lo;
+    const uint32_t po = phase16(out + o);
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t i = threadIdx.x + j * kMergeThreads;
-        if (i < cnt) {
-            __stcs(out + o + i, s_k[i]);
-            if constexpr (VALS) __stcs(vout + o + i, s_v[i]);
+        if (diag + j < cnt) s_k[po + threadIdx.x * ITEMS + j] = rk[j];
+    }
+    uint32_t pvo = 0;
+    if constexpr (VALS) {
+        pvo = phase16(vout + o);
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (diag + j < cnt) s_v[pvo + threadIdx.x * ITEMS + j] = rv[j];
         }
+    }
+    __syncthreads();
+    {
+        T* g = out + o;
+        const uint32_t head = std::min<uint32_t>((V - po) % V, cnt);
+        const uint32_t nv = (cnt - head) / V;
+        const uint32_t tail0 = head + nv * V;
+        for (uint32_t v = threadIdx.x; v < nv; v += kMergeThreads)
+            __stcs(reinterpret_cast<uint4*>(g + head + v * V),
+                   *reinterpret_cast<const uint4*>(s_k + po + head + v * V));
+        const uint32_t th = threadIdx.x;
+        if (th < head) __stcs(g + th, s_k[po + th]);
+        else if (th >= V && th - V < cnt - tail0) __stcs(g + tail0 + (th - V), s_k[po + tail0 + (th - V)]);
+    }
+    if constexpr (VALS) {
+        uint32_t* g = vout + o;
+        const uint32_t head = std::min<uint32_t>((4 - pvo) % 4, cnt);
+        const uint32_t nv = (cnt - head) / 4;
+        const uint32_t tail0 = head + nv * 4;
+        for (uint32_t v = threadIdx.x; v < nv; v += kMergeThreads)
+            __stcs(reinterpret_cast<uint4*>(g + head + v * 4),
+                   *reinterpret_cast<const uint4*>(s_v + pvo + head + v * 4));
+        const uint32_t th = threadIdx.x;
+        if (th < head) __stcs(g + th, s_v[pvo + th]);
+        else if (th >= 4 && th - 4 < cnt - tail0) __stcs(g + tail0 + (th - 4), s_v[pvo + tail0 + (th - 4)]);
     }
 }
 
