@@ -31,6 +31,8 @@ void clear_error();
 // every kernel launch of the library is counted (b2s_kernel_launches)
 void note_launch();
 unsigned long long launch_count();
+void unnote_launches(unsigned long long n);  // launches recorded while capturing a graph
+unsigned long long alloc_generation();       // bumped by every device scratch (re)allocation
 #define B2S_LAUNCHED()                      \
     do {                                    \
         ::b2s::note_launch();               \
@@ -133,6 +135,15 @@ struct b2s_ctx {
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> side_done;
     cudaEvent_t fork = nullptr;
+    // small partitioned sorts are bound by their chain of launches: the second
+    // identical call (same buffers, sizes, p) is captured as a CUDA graph and
+    // later ones replay it (b2s_partitioned_sort)
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t g_in = nullptr, g_out = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    unsigned long long gkey[8] = {}, gseen[8] = {};
+    bool gkey_valid = false, gseen_valid = false;
+    unsigned long long glaunches = 0;  // kernels in the captured graph
 
     bool timing = false;
     cudaEvent_t ev[40] = {};

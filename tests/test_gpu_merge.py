@@ -160,3 +160,34 @@ def test_repeated_calls_see_new_data(ctx, dt):
         if it == 3:  # grow every scratch buffer
             big = to_dev(rand_keys(3 * n, dt, rng))
             ctx.partitioned_sort(big, p)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_partitioned_sort_graph_replay(ctx, dt):
+    """Small partitioned sorts replay a captured CUDA graph from the second
+    identical call on: every call sorts the buffers' current contents, a
+    replay launches the captured kernels (counted), and a call of another
+    shape or after scratch reallocation takes the direct path again."""
+    from paper_1105_6040_b200._lib import lib
+    rng = np.random.default_rng(21)
+    n, p = 1 << 20, 4
+    d_in = to_dev(rand_keys(n, dt, rng))
+    d_out = torch.empty_like(d_in)
+    counts = []
+    for it in range(6):
+        keys = rand_keys(n, dt, rng, ("uniform", "dups", "sorted", "skewed", "equal", "reverse")[it])
+        d_in.copy_(to_dev(keys))
+        l0 = lib().b2s_kernel_launches()
+        ctx.partitioned_sort(d_in, p, out=d_out)
+        counts.append(lib().b2s_kernel_launches() - l0)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_host(d_out, dt), oracle.sort(keys)), it
+        if it == 3:  # another shape, then a scratch reallocation, in between
+            other = to_dev(rand_keys(n // 2, dt, rng))
+            o2, _ = ctx.partitioned_sort(other, 3)
+            big = to_dev(rand_keys(4 * n, dt, rng))
+            ctx.partitioned_sort(big, p)
+            torch.cuda.synchronize()
+            assert np.array_equal(to_host(o2, dt), oracle.sort(to_host(other, dt)))
+    assert all(c > 0 for c in counts), counts
+    assert counts[2] == counts[3] == counts[0], counts  # replays count the captured kernels
