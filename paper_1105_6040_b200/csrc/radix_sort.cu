@@ -447,6 +447,12 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_SEP
 #define B2S_SEP 1
 #endif
+#ifndef B2S_LB_STEP
+#define B2S_LB_STEP 4
+#endif
+#ifndef B2S_LB_PRE
+#define B2S_LB_PRE 2  // measured per 2^28 u32 pass: 2: 0.719 ms, 4: 0.723, 8: 0.98 (smem)
+#endif
 #ifndef B2S_TMA_EVICT_FIRST
 #define B2S_TMA_EVICT_FIRST 1
 #endif
@@ -622,7 +628,7 @@ struct TileShared {
     uint32_t start[kRadix];
     uint32_t wsum[kRadix / 32];
     unsigned long long wsum64[kRadix / 32];
-    alignas(16) LB lbw[4 * kRadix];  // prefetched look-back window
+    alignas(16) LB lbw[B2S_LB_PRE * kRadix];  // prefetched look-back window
     uint32_t tile[2];
     uint32_t dummy[32];  // sink of the non-leaders' no-op rank atomics
     alignas(8) unsigned long long mbar[2];
@@ -725,8 +731,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     using OFF = typename TileShared<LB>::OFF;
     constexpr int WARPS = THREADS / 32;
     constexpr int WSEG = 32 * ITEMS;
-    constexpr int LOOKBACK = 4;   // predecessors read per synchronous look-back step
-    constexpr int PRE = 4;        // predecessors prefetched before ranking
+    constexpr int LOOKBACK = B2S_LB_STEP;  // predecessors read per synchronous look-back step
+    constexpr int PRE = B2S_LB_PRE;        // predecessors prefetched before ranking
     constexpr int HALF = kRadix / 2;
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
