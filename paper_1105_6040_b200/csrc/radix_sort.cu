@@ -447,6 +447,9 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_SEP
 #define B2S_SEP 1
 #endif
+#ifndef B2S_ARITH_MIN_RANK
+#define B2S_ARITH_MIN_RANK 3  // 2 (regular kernel too): 0.750 vs 0.720 ms per 2^28 u32 pass
+#endif
 #ifndef B2S_LB_STEP
 #define B2S_LB_STEP 4
 #endif
@@ -1220,7 +1223,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     // sort: regular kernel 3.455 ms with the array vs 3.535 ms arithmetic
     // (register allocation), twins faster arithmetic (sorted 2^27: 1.75 ->
     // 1.63 ms, Zipf 1.52 -> 1.48 ms).
-    constexpr bool ARITH = RANK >= 3;
+    constexpr bool ARITH = RANK >= B2S_ARITH_MIN_RANK;
     struct Bufs {
         unsigned char* base;
         U* arr[2];
