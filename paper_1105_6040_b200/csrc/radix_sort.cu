@@ -2088,6 +2088,7 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
 #else
     if constexpr (sizeof(U) == 4 && VALS) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
@@ -2095,16 +2096,24 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
         if (cfg == 4) return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 22, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 11) return launch_passes_cfg<U, VALS, LB, 1024, 24, 1>(ctx, plan, ctr, n, lb);
         if (cfg == 9 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 24>(ctx, plan, ctr, n, lb);
         if (cfg == 10 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 20>(ctx, plan, ctr, n, lb);
         if (cfg == 6) return launch_pipe_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 8) return launch_pipe_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
+        // 8-byte keys + payload: one 1024-thread CTA per SM with 8192-pair
+        // tiles (per 2^28-pair pass 1.92 ms vs 1.97 for two 512-thread CTAs
+        // with 4096-pair tiles, cfg 3; the other key types measured faster
+        // with two CTAs: u32 0.72 vs 0.79, u32+payload 1.33 vs 1.37, u64 1.27
+        // vs 1.32 ms, tools/cfgab.sh)
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 1024, 8, 1>(ctx, plan, ctr, n, lb);
     } else {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
+        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     }
 #endif

@@ -113,7 +113,7 @@ def test_sort_in_place_and_host_buffers(ctx, dt):
 
 @pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("kind", ["dups", "uniform", "equal", "skewed", "sorted", "reverse"])
-@pytest.mark.parametrize("n", [123_457, 3072, 5121, 1])
+@pytest.mark.parametrize("n", [123_457, 3072, 5121, 1, 8191, 8192, 8193, 16385])
 def test_sort_pairs_stable(ctx, dt, kind, n):
     rng = np.random.default_rng(17)
     keys = rand_keys(n, dt, rng, kind)
