@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <map>
 #include <string>
 #include <vector>
@@ -27,6 +28,13 @@ void clear_error();
                                     "%s:%d %s -> %s", __FILE__, __LINE__, #call,         \
                                     cudaGetErrorString(e_));                             \
     } while (0)
+
+// One-time setup per device: kernel attributes (opt-in shared memory) are set
+// per device, so a process driving several GPUs sets them on each.
+inline bool first_on_device(std::atomic<unsigned long long>& mask, int device) {
+    const unsigned long long bit = 1ull << (device & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
+}
 
 // every kernel launch of the library is counted (b2s_kernel_launches)
 void note_launch();

@@ -494,12 +494,10 @@ template <typename T, bool VALS>
 b2s_status launch_groups(b2s_ctx* ctx, const KRuns<T>& R, const uint64_t* cuts, uint64_t ngroups,
                          T* out, uint32_t* vout) {
     auto kern = kmerge_group_kernel<T, VALS>;
-    static bool init = false;
-    if (!init) {
+    static std::atomic<unsigned long long> set_on{0};
+    if (first_on_device(set_on, ctx->device))
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)group_smem<T, VALS>(group_cap<T, VALS>(kMaxK))));
-        init = true;
-    }
     const uint32_t cap = group_cap<T, VALS>(R.k);
     kern<<<(unsigned)ngroups, kKThreads, group_smem<T, VALS>(cap), ctx->stream>>>(R, cuts, cap, out, vout);
     B2S_LAUNCHED();

@@ -1950,8 +1950,9 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
     const Kern kern[3] = {onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>,
                           onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 3>,
                           onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 4>};
-    static int occ[3] = {-1, -1, -1};  // per instantiation, per process (single device type)
-    if (occ[0] < 0) {
+    static int occ[3] = {-1, -1, -1};  // per instantiation (one device type)
+    static std::atomic<unsigned long long> set_on{0};
+    if (first_on_device(set_on, ctx->device)) {
         for (int k = 0; k < NK; ++k) {
             B2S_CUDA(cudaFuncSetAttribute(kern[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)SMEM));
@@ -2013,7 +2014,8 @@ b2s_status launch_pipe_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
     constexpr size_t SMEM = SM::bytes;
     auto kern = onesweep_pipe_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>;
     static int occ = -1;
-    if (occ < 0) {
+    static std::atomic<unsigned long long> set_on{0};
+    if (first_on_device(set_on, ctx->device)) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
         int o = 0;
         B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
@@ -2048,7 +2050,8 @@ b2s_status launch_ws_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
     constexpr size_t SMEM = SM::bytes;
     auto kern = onesweep_ws_kernel<U, VALS, LB, ITEMS>;
     static int occ = -1;
-    if (occ < 0) {
+    static std::atomic<unsigned long long> set_on{0};
+    if (first_on_device(set_on, ctx->device)) {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
         int o = 0;
         B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 512, SMEM));
@@ -2147,12 +2150,10 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     // pairs' passes gain nothing from skipping the in-pass count (1.96 ms)
     const bool all_hist = n >= kAllHistMinKeys && all_hist_mode() >= (sizeof(U) == 4 ? 1 : 2);
     if (all_hist) {
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> set_on{0};
+        if (first_on_device(set_on, ctx->device))
             B2S_CUDA(cudaFuncSetAttribute(radix_prologue_all_kernel<U>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAllHistSmem));
-            attr = true;
-        }
         const uint64_t want = (n / (16 / sizeof(U)) + kAllHistThreads * 4 - 1) / (kAllHistThreads * 4);
         const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)ctx->num_sms);
         radix_prologue_all_kernel<U><<<grid, kAllHistThreads, kAllHistSmem, ctx->stream>>>(

@@ -154,13 +154,11 @@ b2s_status select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count, 
     int m = 1;
     while (m < count) m <<= 1;
     const size_t smem = (size_t)m * sizeof(b2s_sample);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> set_on{0};
+    if (first_on_device(set_on, ctx->device))
         B2S_CUDA(cudaFuncSetAttribute(select_splitters_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(kSelectMax * sizeof(b2s_sample))));
-        attr = true;
-    }
     select_splitters_kernel<<<1, 1024, smem, ctx->stream>>>(samples, count, nparts, splitters);
     B2S_LAUNCHED();
     return B2S_OK;
