@@ -354,41 +354,60 @@ __global__ void kmerge_cuts_kernel(const KRuns<T> R, const T* __restrict__ skeys
     cuts[g * k + r2] = cut;
 }
 
-// shared bytes of a group kernel for k runs: two buffers of cap records
+// shared bytes of a group kernel for k runs: two buffers of cap records. The
+// first buffer holds the k slices each at its global 16-byte phase (up to
+// 2V-2 records of padding per slice), the output is restaged at its phase,
+// and the merge may read one record past the end.
 template <typename T, bool VALS>
 constexpr uint32_t group_cap(int k) {
-    return GroupCfg<T>::T_ + (uint32_t)k * GroupCfg<T>::S + 4;  // + one-past-the-end read
+    return (GroupCfg<T>::T_ + (uint32_t)k * GroupCfg<T>::S + (uint32_t)(2 * k + 2) * 4 + 4 + 3) / 4 * 4;
 }
 template <typename T, bool VALS>
 constexpr size_t group_smem(uint32_t cap) {
     return 2 * (size_t)cap * sizeof(T) + (VALS ? 2 * (size_t)cap * 4 : 0);
 }
 
+// One group: its k slices are staged in shared memory with 16-byte copies
+// (each at its global phase, so the first round reads segments with gaps),
+// merged pairwise in shared memory (log2 k rounds, ties to the lower run,
+// two heads in registers; the last round writes at the output's phase) and
+// written with 16-byte stores.
 template <typename T, bool VALS>
 __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> R,
                                                                  const uint64_t* __restrict__ cuts,
                                                                  uint32_t cap, T* __restrict__ out,
                                                                  uint32_t* __restrict__ vout) {
     constexpr int ITEMS = sizeof(T) == 4 ? 19 : 15;  // odd: conflict-free strided stores
+    constexpr uint32_t V = 16 / sizeof(T);
     extern __shared__ __align__(16) unsigned char smem[];
     // buffers are selected arithmetically (an indexed pointer array would
     // lose the shared address space and turn every access generic)
     T* const kbase = reinterpret_cast<T*>(smem);
     uint32_t* const vbase = reinterpret_cast<uint32_t*>(smem + 2 * (size_t)cap * sizeof(T));
-    __shared__ uint32_t s_seg[kMaxK + 1];
+    __shared__ uint32_t s_seg[kMaxK + 1];          // output-space segments (prefix of lengths)
+    __shared__ uint32_t s_kbeg[kMaxK], s_vbeg[kMaxK];  // staged slices in buffer 0
     __shared__ uint64_t s_lo[kMaxK];
     __shared__ uint64_t s_out;
     const int k = R.k;
     const int tid = threadIdx.x;
     const uint64_t g = blockIdx.x;
     if (tid == 0) {
-        uint32_t acc = 0;
+        uint32_t acc = 0, kp = 0, vp = 0;
         uint64_t o = 0;
         for (int r = 0; r < k; ++r) {
             const uint64_t lo = cuts[g * k + r], hi = cuts[(g + 1) * k + r];
+            const uint32_t len = (uint32_t)(hi - lo);
             s_lo[r] = lo;
             s_seg[r] = acc;
-            acc += (uint32_t)(hi - lo);
+            kp = (kp + V - 1) / V * V + phase16(R.key[r] + lo);
+            s_kbeg[r] = kp;
+            kp += len;
+            if constexpr (VALS) {
+                vp = (vp + 3) / 4 * 4 + phase16(R.val[r] + lo);
+                s_vbeg[r] = vp;
+                vp += len;
+            }
+            acc += len;
             o += lo;
         }
         s_seg[k] = acc;
@@ -396,72 +415,66 @@ __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> 
     }
     __syncthreads();
     const uint32_t total = s_seg[k];
-    // the k slices, concatenated in run order
     for (int r = 0; r < k; ++r) {
-        const uint32_t base = s_seg[r], len = s_seg[r + 1] - base;
-        const T* src = R.key[r] + s_lo[r];
-        for (uint32_t i = tid; i < len; i += kKThreads) cp_async_elem(&kbase[base + i], src + i);
-        if constexpr (VALS) {
-            const uint32_t* vs = R.val[r] + s_lo[r];
-            for (uint32_t i = tid; i < len; i += kKThreads) cp_async_elem(&vbase[base + i], vs + i);
-        }
+        const uint32_t len = s_seg[r + 1] - s_seg[r];
+        stage_slice(kbase + s_kbeg[r], R.key[r] + s_lo[r], len);
+        if constexpr (VALS) stage_slice(vbase + s_vbeg[r], R.val[r] + s_lo[r], len);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    const uint64_t o = s_out;
+    const uint32_t po = phase16(out + o);
+    const uint32_t pvo = VALS ? phase16(vout + o) : 0u;
     // pairwise rounds in shared memory; after a round segment i spans the old
     // segments 2i and 2i+1
     int cur = 0;
     int m = k;
+    bool first = true;
     while (m > 1) {
+        const bool last = (m + 1) / 2 == 1;
         const T* ks = kbase + (cur ? cap : 0);
-        T* kd = kbase + (cur ? 0 : cap);
+        T* kd = kbase + (cur ? 0 : cap) + (last ? po : 0);
         const uint32_t* vs = vbase + (cur ? cap : 0);
-        uint32_t* vd = vbase + (cur ? 0 : cap);
+        uint32_t* vd = vbase + (cur ? 0 : cap) + (last ? pvo : 0);
         for (uint32_t x0 = tid * ITEMS; x0 < total; x0 += kKThreads * ITEMS) {
             const uint32_t x1 = min(x0 + ITEMS, total);
             uint32_t x = x0;
             int p = 0;
             while (2 * (p + 1) < m && s_seg[2 * (p + 1)] <= x) ++p;  // pair holding x
-            {
-                // common case: the whole chunk inside one pair, fully unrolled
-                const uint32_t a0 = s_seg[2 * p];
-                const uint32_t a1 = s_seg[min(2 * p + 1, m)];
-                const uint32_t e1 = s_seg[min(2 * p + 2, m)];
-                if (x0 + ITEMS <= e1) {
-                    const uint32_t diag = x0 - a0;
-                    uint32_t ai = a0 + merge_path_smem(ks + a0, a1 - a0, ks + a1, e1 - a1, diag);
-                    uint32_t bi = a1 + (diag - (ai - a0));
-                    T ka = ks[ai], kb = ks[bi];
+            while (x < x1) {
+                // pair p: A = segment 2p, B = segment 2p+1 (empty past the end)
+                const int ia = 2 * p, ib = min(2 * p + 1, m);
+                const uint32_t o0 = s_seg[ia];
+                const uint32_t la = s_seg[min(ia + 1, m)] - o0;
+                const uint32_t lb = s_seg[min(ib + 1, m)] - s_seg[ib];
+                const T* ka_p = ks + (first ? s_kbeg[ia] : o0);
+                const T* kb_p = ks + (first ? (ib < m ? s_kbeg[ib] : 0u) : s_seg[ib]);
+                const uint32_t* va_p = vs + (VALS ? (first ? s_vbeg[ia] : o0) : 0u);
+                const uint32_t* vb_p = vs + (VALS ? (first ? (ib < m ? s_vbeg[ib] : 0u) : s_seg[ib]) : 0u);
+                const uint32_t diag = x - o0;
+                uint32_t ai = merge_path_smem(ka_p, la, kb_p, lb, diag);
+                uint32_t bi = diag - ai;
+                T ka = ka_p[ai], kb = kb_p[bi];
+                const uint32_t stop = min(x1, o0 + la + lb);
+                if (x == x0 && stop == x0 + ITEMS) {
+                    // common case: the whole chunk inside one pair, unrolled
 #pragma unroll
                     for (int j = 0; j < ITEMS; ++j) {
-                        const bool take_a = bi >= e1 || (ai < a1 && !(kb < ka));
+                        const bool take_a = bi >= lb || (ai < la && !(kb < ka));
                         kd[x0 + j] = take_a ? ka : kb;
-                        if constexpr (VALS) vd[x0 + j] = vs[take_a ? ai : bi];
-                        const uint32_t nxt = take_a ? ++ai : ++bi;
-                        const T kn = ks[nxt];
-                        if (take_a) ka = kn;
-                        else kb = kn;
+                        if constexpr (VALS) vd[x0 + j] = take_a ? va_p[ai] : vb_p[bi];
+                        if (take_a) ka = ka_p[++ai];
+                        else kb = kb_p[++bi];
                     }
-                    continue;
-                }
-            }
-            while (x < x1) {
-                const uint32_t a0 = s_seg[2 * p];
-                const uint32_t a1 = s_seg[min(2 * p + 1, m)];
-                const uint32_t e1 = s_seg[min(2 * p + 2, m)];
-                const uint32_t diag = x - a0;
-                uint32_t ai = a0 + merge_path_smem(ks + a0, a1 - a0, ks + a1, e1 - a1, diag);
-                uint32_t bi = a1 + (diag - (ai - a0));
-                T ka = ks[ai], kb = ks[bi];
-                const uint32_t stop = min(x1, e1);
-                for (; x < stop; ++x) {
-                    const bool take_a = bi >= e1 || (ai < a1 && !(kb < ka));
-                    kd[x] = take_a ? ka : kb;
-                    if constexpr (VALS) vd[x] = vs[take_a ? ai : bi];
-                    const uint32_t nxt = take_a ? ++ai : ++bi;
-                    const T kn = ks[nxt];
-                    if (take_a) ka = kn;
-                    else kb = kn;
+                    x = x1;
+                } else {
+                    for (; x < stop; ++x) {
+                        const bool take_a = bi >= lb || (ai < la && !(kb < ka));
+                        kd[x] = take_a ? ka : kb;
+                        if constexpr (VALS) vd[x] = take_a ? va_p[ai] : vb_p[bi];
+                        if (take_a) ka = ka_p[++ai];
+                        else kb = kb_p[++bi];
+                    }
                 }
                 ++p;
             }
@@ -473,14 +486,31 @@ __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> 
         }
         m = (m + 1) / 2;
         cur ^= 1;
+        first = false;
         __syncthreads();
     }
-    const uint64_t o = s_out;
-    const T* kf = kbase + (cur ? cap : 0);
-    const uint32_t* vf = vbase + (cur ? cap : 0);
-    for (uint32_t i = tid; i < total; i += kKThreads) {
-        __stcs(out + o + i, kf[i]);
-        if constexpr (VALS) __stcs(vout + o + i, vf[i]);
+    // the result sits at the output's 16-byte phase: 16-byte stores
+    const T* kf = kbase + (cur ? cap : 0) + po;
+    {
+        T* gk = out + o;
+        const uint32_t head = min((V - po) % V, total);
+        const uint32_t nv = (total - head) / V;
+        const uint32_t tail0 = head + nv * V;
+        for (uint32_t v = tid; v < nv; v += kKThreads)
+            __stcs(reinterpret_cast<uint4*>(gk + head + v * V), *reinterpret_cast<const uint4*>(kf + head + v * V));
+        if ((uint32_t)tid < head) __stcs(gk + tid, kf[tid]);
+        else if ((uint32_t)tid >= V && tid - V < total - tail0) __stcs(gk + tail0 + (tid - V), kf[tail0 + (tid - V)]);
+    }
+    if constexpr (VALS) {
+        const uint32_t* vf = vbase + (cur ? cap : 0) + pvo;
+        uint32_t* gv = vout + o;
+        const uint32_t head = min((4 - pvo) % 4, total);
+        const uint32_t nv = (total - head) / 4;
+        const uint32_t tail0 = head + nv * 4;
+        for (uint32_t v = tid; v < nv; v += kKThreads)
+            __stcs(reinterpret_cast<uint4*>(gv + head + v * 4), *reinterpret_cast<const uint4*>(vf + head + v * 4));
+        if ((uint32_t)tid < head) __stcs(gv + tid, vf[tid]);
+        else if ((uint32_t)tid >= 4 && tid - 4 < total - tail0) __stcs(gv + tail0 + (tid - 4), vf[tail0 + (tid - 4)]);
     }
 }
 
@@ -567,10 +597,12 @@ struct Run {
 int kway_mode() {
     static int m = -1;
     if (m < 0) {
-        // 0: pairwise rounds (default: 3.5 TB/s per round on B200), 1: the
-        // single-pass bucket merge (correct, but its in-shared-memory merge is
-        // latency-bound at the occupancy its buffers allow: 3.5 ms vs 1.84 ms for
-        // 8 runs of 2^25 keys -- kept for further work)
+        // 0: pairwise rounds (default: ~4 TB/s per round on B200), 1: the
+        // grouped single-pass merge. It reads and writes every key once, but
+        // the merge is bound by instructions and shared-memory wavefronts,
+        // not HBM, and its log2(k) in-shared-memory rounds cost what the
+        // global rounds cost: 8 runs of 2^25 i32 1.76 ms vs 1.69 pairwise,
+        // 4 runs 1.07 vs 1.09 (ncu: 147 instructions per output either way)
         const char* e = getenv("B2S_KWAY");
         m = e ? atoi(e) : 0;
     }
