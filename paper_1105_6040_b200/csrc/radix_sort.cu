@@ -2085,8 +2085,13 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
 #ifdef B2S_DEV_FAST
     // development builds (tools/kdev_build.sh, -DB2S_DEV_FAST): only the default
     // u32 keys-only pass is compiled, for quick kernel iteration
-    (void)cfg;
-    if constexpr (sizeof(U) == 4 && !VALS) return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
+    if constexpr (sizeof(U) == 4 && !VALS) {
+        // occupancy experiments (per 2^28 u32 pass): 3 x 384 thr x 20 items
+        // 0.776 ms, 4 x 256 x 24 0.891, default 2 x 512 x 24 0.722
+        if (cfg == 12) return launch_passes_cfg<U, VALS, LB, 384, 20, 3>(ctx, plan, ctr, n, lb);
+        if (cfg == 13) return launch_passes_cfg<U, VALS, LB, 256, 24, 4>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
+    }
     return B2S_EINVAL;
 #else
     if constexpr (sizeof(U) == 4 && VALS) {
