@@ -465,6 +465,12 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_EARLY_LB
 #define B2S_EARLY_LB 0
 #endif
+#ifndef B2S_ECNT_IN_CNT
+#define B2S_ECNT_IN_CNT 1
+#endif
+#ifndef B2S_NAMED_SCAN
+#define B2S_NAMED_SCAN 1
+#endif
 #ifndef B2S_ERANK_RELOAD
 #define B2S_ERANK_RELOAD 1
 #endif
@@ -783,7 +789,11 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // into separate words with +1 increments (ATOMS.POPC.INC aggregates lanes
     // that hit the same counter); the digit section packs them into 16-bit
     // pairs for ranking.
-    uint32_t* ecnt = s_early + warp * kRadix;
+    // RANK 5/6 (B2S_ECNT_IN_CNT): the packed early counts live in the warp's
+    // own s_cnt segment (the digit section turns them into its lookup table in
+    // place), so no other warp's data shares their words
+    constexpr bool ECNT = ER && B2S_ECNT_IN_CNT;
+    uint32_t* ecnt = ECNT ? s_cnt + warp * HALF : s_early + warp * kRadix;
     if constexpr (!PIPE) {
         // the counts live in the idle tile buffer (nothing streams into it
         // before this tile's look-back is done); each warp clears its own 1 KB
@@ -856,6 +866,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             if (FULL || wbase + j * 32 + lane < tile_valid) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
         }
     }
+    if constexpr (!PIPE) between();  // regular kernel: publish the next tile id
     __syncthreads();  // also: every warp has read its keys out of kbuf
     B2S_PHASE(1);
 
@@ -867,7 +878,9 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         for (int w = 0; w < WARPS; ++w) {
             uint32_t* e = s_early + w * kRadix;
             uint32_t c;
-            if constexpr (ER) {
+            if constexpr (ECNT) {
+                c = s_cnt[w * HALF + tid];  // packed pair, replaced by the prefix below
+            } else if constexpr (ER) {
                 c = e[tid];  // packed pair; the region is cleared at the next tile's start
             } else {
                 c = e[tid] | (e[HALF + tid] << 16);
@@ -905,7 +918,16 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    __syncthreads();
+    // RANK 5/6: only the four scanning warps wait for each other here (named
+    // barrier); the others go on to re-read their keys, and one full barrier
+    // after the re-read covers both the finished digit section and the
+    // in-place staging
+    constexpr bool NAMED = ER && B2S_ERANK_RELOAD && B2S_NAMED_SCAN;
+    if constexpr (NAMED) {
+        if (tid < HALF) asm volatile("bar.sync 1, %0;" ::"n"(HALF) : "memory");
+    } else {
+        __syncthreads();
+    }
     if (tid < HALF) {
         uint32_t base = 0;
 #pragma unroll
@@ -917,7 +939,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #pragma unroll 4
         for (int w = 0; w < WARPS; ++w) s_cnt[w * HALF + tid] += add;
     }
-    __syncthreads();
+    if constexpr (!NAMED) __syncthreads();
     // ---- decoupled look-back: one lane per digit. The first PRE predecessors
     // were fetched before ranking; later steps read LOOKBACK at a time
     // (independent loads) in a warp-uniform loop. Each lane publishes its
@@ -993,7 +1015,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
 #pragma unroll
             for (int j = 0; j < ITEMS; ++j) vals[j] = vbuf[wbase + j * 32 + lane];
         }
-        if constexpr (!SEP) __syncthreads();  // in-place staging: all reads first
+        // in-place staging: all reads first (and with NAMED the digit section's end)
+        if constexpr (!SEP || NAMED) __syncthreads();
     }
 #endif
     if constexpr (ELB) lookback();
@@ -1314,10 +1337,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         const uint32_t tile = sh.tile[cur];
         if (tile >= ntiles) break;
         // claim the next tile and stream it in during this tile's write-out
-        // (by a thread that sits out the look-back)
-        auto noop = []() {};
-        // the next tile id is fetched now (its atomic's latency hides behind
-        // this tile) but published and prefetched only after the look-back
+        // (by a thread that sits out the look-back); the id is fetched now
+        // (its atomic's latency hides behind the early counts)
         uint32_t next_t = 0;
         if (tid == THREADS - 1) next_t = atomicAdd(&plan->tile_counter[slot], 1u);
         // SEP: tiles always land in buffer 0 and are staged in buffer 1
@@ -1325,11 +1346,14 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         // each tile is staged in place
         const int lb_ = SEP ? 0 : cur;
         const int sb_ = SEP ? 1 : cur;
+        // the next tile id is published before the early-count barrier (so
+        // every thread knows it at this tile's end), its copy is issued after
+        // the look-back (the buffer is free then)
+        auto publish = [&]() {
+            if (tid == THREADS - 1) sh.tile[cur ^ 1] = next_t;
+        };
         auto claim = [&]() {
-            if (tid == THREADS - 1) {
-                sh.tile[cur ^ 1] = next_t;
-                prefetch(next_t, SEP ? 0 : cur ^ 1);
-            }
+            if (tid == THREADS - 1) prefetch(next_t, SEP ? 0 : cur ^ 1);
         };
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
@@ -1341,19 +1365,32 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 parity ^= 1u << lb_;
                 B2S_PHASE(0);
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR, SWZ, SEP>(
-                    claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
+                    claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR, SWZ, SEP>(
-                    claim, noop, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
+                    claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
             }
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR, SWZ, SEP>(
-                claim, noop, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
+                claim, publish, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
                 nd, s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
         }
-        __syncthreads();
+        // Between two full TMA tiles of the early-rank kernels no barrier is
+        // needed: the next tile's early counts go to each warp's own s_cnt
+        // segment and it lands in the other buffer, and its first barrier
+        // (after the early counts) is only passed once every warp has
+        // finished this write-out. Any other next tile (partial: early counts
+        // in this staging buffer; none: the CTA's final reductions) waits.
+        {
+            bool skip = false;
+            if constexpr ((TR == 5 || TR == 6) && B2S_ECNT_IN_CNT && B2S_ERANK_RELOAD) {
+                const uint32_t nt = sh.tile[cur ^ 1];
+                skip = tma && nt < ntiles && n - (uint64_t)nt * TILE >= (uint64_t)TILE;
+            }
+            if (!skip) __syncthreads();
+        }
         B2S_PHASE(5);
         cur ^= 1;
     }
