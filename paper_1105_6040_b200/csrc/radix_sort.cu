@@ -468,6 +468,9 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_ECNT_IN_CNT
 #define B2S_ECNT_IN_CNT 1
 #endif
+#ifndef B2S_EARLY_CLAIM
+#define B2S_EARLY_CLAIM 0  // 1: next tile streamed in after the early counts: 0.709 vs 0.699 ms per pass
+#endif
 #ifndef B2S_NAMED_SCAN
 #define B2S_NAMED_SCAN 1
 #endif
@@ -869,6 +872,12 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     if constexpr (!PIPE) between();  // regular kernel: publish the next tile id
     __syncthreads();  // also: every warp has read its keys out of kbuf
     B2S_PHASE(1);
+    // With the early counts in s_cnt the other tile buffer holds nothing but
+    // the previous tile's staged keys, all written out once every warp has
+    // passed the barrier above: the next tile streams in from here on (else
+    // after the look-back). Separate staging buffers: after the key re-read.
+    constexpr bool EARLY_CLAIM = ECNT && B2S_EARLY_CLAIM;
+    if constexpr (EARLY_CLAIM && !SEP) claim_next();
 
     // ---- per digit pair (thread t < 128 owns digits 2t, 2t+1): exclusive
     // prefix over warps, tile counts, publish them at once
@@ -1017,6 +1026,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         }
         // in-place staging: all reads first (and with NAMED the digit section's end)
         if constexpr (!SEP || NAMED) __syncthreads();
+        if constexpr (EARLY_CLAIM && SEP) claim_next();
     }
 #endif
     if constexpr (ELB) lookback();
@@ -1168,7 +1178,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     if constexpr (PIPE) return;  // the caller syncs; this tile is written next round
     __syncthreads();
     B2S_PHASE(4);
-    claim_next();
+    if constexpr (!EARLY_CLAIM) claim_next();
 
     // ---- write runs of equal digits; clear this warp's counters (RANK 5
     // overwrites them in the digit section)
