@@ -149,6 +149,17 @@ b2s_status b2s_partitioned_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, v
  * partitions get one extra key. sizes has p slots (host). */
 b2s_status b2s_plan_partition(uint64_t n, int p, uint64_t* sizes);
 
+/* The reference's own p-phase algorithm on one device, for comparison with
+ * the merge of b2s_partitioned_sort: plan_partition scatter, a radix sort of
+ * each block, p odd-even phases of merge_split_padded at width ceil(n/p)
+ * between partner blocks (build_schedule, P/src/parallel_sort.cpp:40-55,
+ * 217-244; every merge-split is a merge-path window on the device, the kept
+ * counts follow from the widths on the host, so nothing synchronises), and
+ * the rank-order gather into `out` (:246-248). Keys only, like the
+ * reference. p >= 1. */
+b2s_status b2s_odd_even_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, void* out, uint64_t n,
+                             int p, uint32_t flags);
+
 /* ---- odd-even merge-split (the reference's own exchange step) -----------
  * merge_split_padded (P/src/parallel_sort.cpp:115-134) on the device: `mine`
  * and `theirs` are sorted runs padded with virtual top sentinels to the same

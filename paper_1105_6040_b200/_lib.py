@@ -20,7 +20,8 @@ B2S_DEVICE, B2S_HOST = 0, 1
 EXPORTS = [
     "b2s_create", "b2s_destroy", "b2s_set_stream", "b2s_synchronize", "b2s_enable_timing",
     "b2s_get_timing", "b2s_last_error", "b2s_version", "b2s_device_count", "b2s_kernel_launches", "b2s_sort",
-    "b2s_merge", "b2s_sort_batch", "b2s_partitioned_sort", "b2s_plan_partition", "b2s_merge_split_padded",
+    "b2s_merge", "b2s_sort_batch", "b2s_partitioned_sort", "b2s_odd_even_sort", "b2s_plan_partition",
+    "b2s_merge_split_padded",
     "b2s_sample_regular", "b2s_select_splitters", "b2s_bucket_bounds", "b2s_gen_keys",
     "b2s_check_sorted", "b2s_exchange_buffer", "b2s_open_peer", "b2s_close_peers",
 ]
@@ -64,6 +65,7 @@ _SIGS = {
     "b2s_merge": (_st, [_p, _i, _p, _p, _p, _i, _p, _p, _u32]),
     "b2s_sort_batch": (_st, [_p, _i, _p, _p, _p, _p, _u64, _i, _u32]),
     "b2s_partitioned_sort": (_st, [_p, _i, _p, _p, _p, _p, _u64, _i, _u32]),
+    "b2s_odd_even_sort": (_st, [_p, _i, _p, _p, _u64, _i, _u32]),
     "b2s_plan_partition": (_st, [_u64, _i, _p]),
     "b2s_merge_split_padded": (_st, [_p, _i, _p, _u64, _u64, _p, _u64, _u64, _i, _p, _p, _p,
                                      _u32]),

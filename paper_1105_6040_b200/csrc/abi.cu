@@ -261,7 +261,7 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
                       &ctx->lookback, &ctx->hist,      &ctx->plan,      &ctx->parts,
                       &ctx->misc,     &ctx->stage_in,  &ctx->stage_out, &ctx->stage_vin,
                       &ctx->stage_vout, &ctx->xbuf, &ctx->seg_lookback, &ctx->seg_hist,
-                      &ctx->seg_plan, &ctx->kmerge};
+                      &ctx->seg_plan, &ctx->kmerge, &ctx->oe_keys};
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
     if (ctx->g_in) cudaEventDestroy(ctx->g_in);
@@ -719,6 +719,70 @@ b2s_status partitioned_sort_dev(b2s_ctx* ctx, b2s_dtype dtype, const void* din, 
 }
 }  // namespace b2s
 }  // extern "C++"
+
+b2s_status b2s_odd_even_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* in, void* out, uint64_t n,
+                             int p, uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (p < 1) return set_error(B2S_EINVAL, "partition needs at least one process");
+    if (n > 0 && (in == nullptr || out == nullptr))
+        return set_error(B2S_EINVAL, "null key buffer with n = %llu", (unsigned long long)n);
+    const size_t ksz = (size_t)key_bytes(dtype);
+    timing_reset(ctx);
+    if (n == 0) return B2S_OK;
+    const void* din = in;
+    void* dout = out;
+    if (flags & B2S_HOST) {
+        B2S_TRY(h2d(ctx, ctx->stage_in, in, n * ksz));
+        din = dout = ctx->stage_in.ptr;
+    }
+    std::vector<uint64_t> sizes(p);
+    b2s_plan_partition(n, p, sizes.data());
+    const uint64_t width = sizes[0];
+    // block r lives in slot r of buffer cur[r] (two buffers of p slots)
+    B2S_TRY(ctx->oe_keys.ensure(2 * (size_t)p * width * ksz + 16));
+    char* buf = static_cast<char*>(ctx->oe_keys.ptr);
+    auto slot = [&](int r, int b) { return buf + ((size_t)b * p + r) * width * ksz; };
+    std::vector<int> cur(p, 0);
+    std::vector<uint64_t> nreal(sizes);
+    uint64_t off = 0;
+    for (int r = 0; r < p; ++r) {  // scatter + local sorts
+        if (sizes[r])
+            B2S_TRY(radix_sort(ctx, dtype, static_cast<const char*>(din) + off * ksz, slot(r, 0), nullptr,
+                               nullptr, sizes[r]));
+        off += sizes[r];
+    }
+    std::vector<uint64_t> nn(p);
+    for (int phase = 0; phase < p; ++phase) {  // build_schedule's pairs
+        for (int r = (phase % 2 == 0) ? 0 : 1; r + 1 < p; r += 2) {
+            const int q = r + 1;
+            uint64_t v = 0;
+            B2S_TRY(merge_split_padded(ctx, dtype, slot(r, cur[r]), nreal[r], width - nreal[r],
+                                       slot(q, cur[q]), nreal[q], width - nreal[q], 0,
+                                       slot(r, 1 - cur[r]), &nn[r], &v));
+            B2S_TRY(merge_split_padded(ctx, dtype, slot(q, cur[q]), nreal[q], width - nreal[q],
+                                       slot(r, cur[r]), nreal[r], width - nreal[r], 1,
+                                       slot(q, 1 - cur[q]), &nn[q], &v));
+        }
+        for (int r = (phase % 2 == 0) ? 0 : 1; r + 1 < p; r += 2) {
+            cur[r] ^= 1;
+            cur[r + 1] ^= 1;
+            nreal[r] = nn[r];
+            nreal[r + 1] = nn[r + 1];
+        }
+    }
+    off = 0;
+    for (int r = 0; r < p; ++r) {  // rank-order gather
+        if (nreal[r])
+            B2S_CUDA(cudaMemcpyAsync(static_cast<char*>(dout) + off * ksz, slot(r, cur[r]), nreal[r] * ksz,
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+        off += nreal[r];
+    }
+    ctx->have_sort = false;
+    ctx->have_merge = true;
+    if (flags & B2S_HOST) B2S_TRY(d2h_sync(ctx, out, dout, n * ksz));
+    return B2S_OK;
+}
 
 b2s_status b2s_merge_split_padded(b2s_ctx* ctx, b2s_dtype dtype, const void* mine,
                                   uint64_t n_mine, uint64_t mine_virtuals, const void* theirs,

@@ -140,6 +140,7 @@ struct b2s_ctx {
     // concurrent local sorts
     b2s::DevBuf seg_lookback, seg_hist, seg_plan;
     b2s::DevBuf kmerge;  // grouped k-way merge: samples, tags, cuts
+    b2s::DevBuf oe_keys;  // odd-even sort: two slots of width ceil(n/p) per block
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> side_done;
     cudaEvent_t fork = nullptr;

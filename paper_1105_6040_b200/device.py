@@ -182,6 +182,20 @@ class Context:
                                          B2S_HOST if host else B2S_DEVICE))
         return out, vals_out
 
+    def odd_even_sort(self, keys, p: int, out=None, stream=None):
+        """The reference's p-phase odd-even merge-split sort on this device
+        (b2s_odd_even_sort), for comparison with partitioned_sort."""
+        _check_1d(keys, "keys")
+        host = _is_host(keys)
+        if out is None:
+            out = np.empty_like(keys) if host else torch.empty_like(keys)
+        self._validate_pair(keys, out, None, None)
+        if not host:
+            self._bind_stream(stream)
+        check(lib().b2s_odd_even_sort(self._h, dtype_code(keys), _ptr(keys), _ptr(out), _numel(keys),
+                                      int(p), B2S_HOST if host else B2S_DEVICE))
+        return out
+
     def merge(self, runs, vals=None, out=None, vals_out=None, stream=None):
         """Stable k-way merge of sorted runs (ties to the lower run index)."""
         if len(runs) == 0:

@@ -191,3 +191,25 @@ def test_partitioned_sort_graph_replay(ctx, dt):
             assert np.array_equal(to_host(o2, dt), oracle.sort(to_host(other, dt)))
     assert all(c > 0 for c in counts), counts
     assert counts[2] == counts[3] == counts[0], counts  # replays count the captured kernels
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 8, 13])
+def test_odd_even_sort(ctx, dt, p):
+    """The reference's own p-phase algorithm on the device (radix-sorted
+    blocks, p odd-even merge_split_padded phases, rank-order gather):
+    bit-exact with the oracle's restatement of scatter_merge_sort (int64) and
+    with the sorted input (other key types)."""
+    rng = np.random.default_rng(100 + p)
+    for n in (0, 5, 4097, 250_001):
+        keys = rand_keys(n, dt, rng, "uniform" if n % 2 else "dups")
+        out = ctx.odd_even_sort(to_dev(keys), p)
+        torch.cuda.synchronize()
+        if dt == np.int64:
+            expect = oracle.scatter_merge_sort(keys, p)
+        else:
+            expect = np.sort(keys)
+        assert np.array_equal(to_host(out, dt), expect), (n, p)
+    # host buffers
+    keys = rand_keys(10_000, dt, rng)
+    assert np.array_equal(ctx.odd_even_sort(keys, p), np.sort(keys))

@@ -88,6 +88,14 @@ def main():
 
     sort_case("cfg1", "N=2^20 i32 p=4 partitioned sort",
               ctx.gen_keys(1 << 20, 1, torch.int32, shift=33), p=4)
+    # the reference's own p-phase algorithm on the device, same input
+    k1 = ctx.gen_keys(1 << 20, 1, torch.int32, shift=33)
+    o1 = torch.empty_like(k1)
+    ms = timed(lambda: ctx.odd_even_sort(k1, 4, out=o1))
+    inv, _, _ = ctx.check_sorted(o1)
+    assert inv == 0
+    record("cfg1", "N=2^20 i32 p=4 odd-even merge-split (the reference's algorithm on the GPU)",
+           1 << 20, ms)
     sort_case("cfg2", "N=2^28 u32", ctx.gen_keys(1 << 28, 1, torch.uint32, shift=32))
 
     # cfg3 per-GPU work at G=8: local sort of a 2^28 shard + merge of 8 runs
