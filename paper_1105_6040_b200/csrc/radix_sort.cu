@@ -2147,7 +2147,10 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
         if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
-        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
+        // small sorts (the partitions of cfg1) are latency-bound: smaller tiles,
+        // more CTAs (2^20 keys, p = 4: 0.088 vs 0.095 ms per partitioned sort)
+        if (cfg == 2 || (cfg == 0 && n < kTwinMinKeys))
+            return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
         if (cfg == 4) return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
         if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 22, 2>(ctx, plan, ctr, n, lb);
