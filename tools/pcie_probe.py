@@ -48,3 +48,30 @@ for chunks in (4, 16):
                 h_out[c * m:(c + 1) * m].copy_(d_b[c * m:(c + 1) * m], non_blocking=True)
     t = run(chunked)
     print(f"both, {chunks} interleaved chunks: {gb / t:.1f} GB/s each direction")
+
+# two copy streams per direction (halves): does a second copy engine help?
+up2, down2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def both_two_engines():
+    m = n // 2
+    for s_up, s_dn, c in ((up, down, 0), (up2, down2, 1)):
+        with torch.cuda.stream(s_up):
+            d_a[c * m:(c + 1) * m].copy_(h_in[c * m:(c + 1) * m], non_blocking=True)
+        with torch.cuda.stream(s_dn):
+            h_out[c * m:(c + 1) * m].copy_(d_b[c * m:(c + 1) * m], non_blocking=True)
+
+
+t = run(both_two_engines)
+print(f"both, two streams per direction: {gb / t:.1f} GB/s each direction")
+
+
+def h2d_two_engines():
+    m = n // 2
+    for s_up, c in ((up, 0), (up2, 1)):
+        with torch.cuda.stream(s_up):
+            d_a[c * m:(c + 1) * m].copy_(h_in[c * m:(c + 1) * m], non_blocking=True)
+
+
+t = run(h2d_two_engines)
+print(f"H2D alone, two streams: {gb / t:.1f} GB/s")
