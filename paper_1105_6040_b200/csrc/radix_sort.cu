@@ -61,19 +61,26 @@ namespace {
 
 constexpr int kRadix = 256;
 
+#ifndef B2S_LB_PRE
+#define B2S_LB_PRE 2  // measured per 2^28 u32 pass: 2: 0.719 ms, 4: 0.723, 8: 0.98 (smem)
+#endif
+
+// kPrefetch: predecessors whose words are prefetched before the ranking. The
+// 64-bit words (n >= 2^30) prefetch one: two would push the static shared
+// memory past the two-CTAs-per-SM budget (2^31 i32 pass 7.8 ms at one CTA/SM).
 template <typename LB>
 struct LookbackWord;
 template <>
 struct LookbackWord<uint32_t> {
     static constexpr uint32_t kAgg = 1u << 30, kInc = 2u << 30, kMask = (1u << 30) - 1;
-    static constexpr int kPrefetch = 4;
+    static constexpr int kPrefetch = B2S_LB_PRE;
     static __device__ __forceinline__ uint32_t flag(uint32_t w) { return w >> 30; }
 };
 template <>
 struct LookbackWord<unsigned long long> {
     static constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62,
                                         kMask = (1ull << 62) - 1;
-    static constexpr int kPrefetch = 4;
+    static constexpr int kPrefetch = 1;
     static __device__ __forceinline__ unsigned long long flag(unsigned long long w) {
         return w >> 62;
     }
@@ -453,9 +460,6 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_LB_STEP
 #define B2S_LB_STEP 4
 #endif
-#ifndef B2S_LB_PRE
-#define B2S_LB_PRE 2  // measured per 2^28 u32 pass: 2: 0.719 ms, 4: 0.723, 8: 0.98 (smem)
-#endif
 #ifndef B2S_TMA_EVICT_FIRST
 #define B2S_TMA_EVICT_FIRST 1
 #endif
@@ -640,7 +644,7 @@ struct TileShared {
     uint32_t start[kRadix];
     uint32_t wsum[kRadix / 32];
     unsigned long long wsum64[kRadix / 32];
-    alignas(16) LB lbw[B2S_LB_PRE * kRadix];  // prefetched look-back window
+    alignas(16) LB lbw[LookbackWord<LB>::kPrefetch * kRadix];  // prefetched look-back window
     uint32_t tile[2];
     uint32_t dummy[32];  // sink of the non-leaders' no-op rank atomics
     alignas(8) unsigned long long mbar[2];
@@ -744,7 +748,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     constexpr int WARPS = THREADS / 32;
     constexpr int WSEG = 32 * ITEMS;
     constexpr int LOOKBACK = B2S_LB_STEP;  // predecessors read per synchronous look-back step
-    constexpr int PRE = B2S_LB_PRE;        // predecessors prefetched before ranking
+    constexpr int PRE = W::kPrefetch;      // predecessors prefetched before ranking
     constexpr int HALF = kRadix / 2;
     const int tid = threadIdx.x;
     const int warp = tid >> 5;

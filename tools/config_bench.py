@@ -98,6 +98,12 @@ def main():
            1 << 20, ms)
     sort_case("cfg2", "N=2^28 u32", ctx.gen_keys(1 << 28, 1, torch.uint32, shift=32))
 
+    # cfg3 at G=1: all 2^31 int32 keys on one GPU (64-bit look-back words)
+    big = ctx.gen_keys(1 << 31, 1, torch.int32, shift=33)
+    sort_case("cfg3", "G=1: N=2^31 i32 on one GPU", big)
+    del big
+    torch.cuda.empty_cache()
+
     # cfg3 per-GPU work at G=8: local sort of a 2^28 shard + merge of 8 runs
     shard = ctx.gen_keys(1 << 28, 1, torch.int32, shift=33)
     sort_case("cfg3", "per-GPU local sort (2^28 i32 shard)", shard)
