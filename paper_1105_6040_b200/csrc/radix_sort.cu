@@ -497,9 +497,10 @@ struct OnesweepSmem {
     static constexpr size_t kKeys = (size_t)TILE * sizeof(U);         // one tile buffer
     static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
     // counters | keys[2] | vals[2]: tile i+1 streams in by TMA while tile i is
-    // ranked in place in its own buffer. The per-warp early counts and match
-    // masks (WARPS x 1 KB) live in the idle tile buffer until the next tile's
-    // copy is issued (after the look-back).
+    // ranked in place in its own buffer. The early-rank kernels count into
+    // s_cnt itself; the others keep their per-warp early counts and match
+    // masks (WARPS x 1 KB) in the idle tile buffer until the next tile's copy
+    // is issued (after the look-back).
     static constexpr size_t bytes = kCnt + 2 * kKeys + 2 * kVals;
     static_assert(kKeys >= (size_t)WARPS * kRadix * 4, "idle tile buffer holds the early counts");
 };
@@ -802,9 +803,9 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     constexpr bool ECNT = ER && B2S_ECNT_IN_CNT;
     uint32_t* ecnt = ECNT ? s_cnt + warp * HALF : s_early + warp * kRadix;
     if constexpr (!PIPE) {
-        // the counts live in the idle tile buffer (nothing streams into it
-        // before this tile's look-back is done); each warp clears its own 1 KB
-        // (RANK 5/6 count packed pairs: only the first 512 B are used)
+        // each warp clears its own counters: 512 B of s_cnt (RANK 5/6, packed
+        // pairs) or 1 KB of the idle tile buffer (nothing streams into it
+        // before this tile's look-back is done)
         uint4* z = reinterpret_cast<uint4*>(ecnt);
         constexpr int ZV = (ER ? HALF : kRadix) / 4;
 #pragma unroll
