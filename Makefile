@@ -50,10 +50,21 @@ variant: $(OBJS)
 	$(NVCC) $(NVFLAGS) $(DEFS) -Xptxas -v -c $(SRC)/$(VSRC).cu -o build/v_$(NAME)/$(VSRC).o 2> build/v_$(NAME)/ptxas.txt || (cat build/v_$(NAME)/ptxas.txt; exit 1)
 	$(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_$(NAME).so build/v_$(NAME)/$(VSRC).o $(filter-out $(OBJ)/$(VSRC).o,$(OBJS)) -lcudart
 
+# comparison / ceiling probes (tools/cub_compare.cu, tools/read_probe.cu)
+tools: build/cub_compare build/read_probe
+
+build/cub_compare: tools/cub_compare.cu
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -std=c++17 $< -o $@
+
+build/read_probe: tools/read_probe.cu
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 $< -o $@
+
 oracle:
 	bash oracle/build_ref.sh
 
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean tools prof

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Refresh every committed measurement of the round on one B200 (run from the
-# repo root on the GPU box):  bash tools/round_profile.sh r01
+# repo root on the GPU box, after `make prof tools` here):  bash tools/round_profile.sh r01
 #   bench line (no profiler), ncu launch list of the same command, the
 #   per-configuration results, the phase split and the CUB comparison.
 p=${1:-r01}
