@@ -200,9 +200,21 @@ SortOutcome scatter_merge_sort(Algorithm algorithm, const DataList& data,
     outcome.sorted.resize(data.size());
     if (data.empty()) return outcome;
     const auto t0 = std::chrono::steady_clock::now();
-    check(b2s_partitioned_sort(ctx(), B2S_I64, data.data(), outcome.sorted.data(), nullptr,
-                               nullptr, data.size(), p, B2S_HOST),
-          "b2s_partitioned_sort");
+    // SORTBENCH_B200_PHASES=1 runs the reference's own p odd-even merge-split
+    // phases on the device (same result, the exchange pattern of the paper);
+    // the default merges the p sorted blocks in log2(p) merge-path rounds
+    static const bool phases = [] {
+        const char* e = std::getenv("SORTBENCH_B200_PHASES");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    if (phases)
+        check(b2s_odd_even_sort(ctx(), B2S_I64, data.data(), outcome.sorted.data(), data.size(), p,
+                                B2S_HOST),
+              "b2s_odd_even_sort");
+    else
+        check(b2s_partitioned_sort(ctx(), B2S_I64, data.data(), outcome.sorted.data(), nullptr,
+                                   nullptr, data.size(), p, B2S_HOST),
+              "b2s_partitioned_sort");
     outcome.world.wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     b2s_timing t{};

@@ -43,3 +43,13 @@ def test_cpp_parity_program():
     r = subprocess.run([PROG], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_parity_program_with_odd_even_phases():
+    """The same reference tests with scatter_merge_sort running the
+    reference's own odd-even merge-split phases on the device."""
+    r = subprocess.run([PROG], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, SORTBENCH_B200_PHASES="1"))
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
