@@ -230,6 +230,24 @@ def test_n_at_least_2p30_uses_64bit_lookback(ctx):
     torch.cuda.empty_cache()
 
 
+def test_max_size_cfg3_on_one_gpu(ctx):
+    """cfg3 at G=1: all 2^31 int32 keys (z >> 33) sorted on one GPU (64-bit
+    look-back words, one prefetched predecessor): sortedness, multiset
+    equality with the input and determinism, checked on the device; the
+    first key is no larger than the smallest of a 2^24-key input sample."""
+    n = 1 << 31
+    keys = ctx.gen_keys(n, 1, torch.int32, shift=33)
+    _, _, ms_in = ctx.check_sorted(keys)
+    out, _ = ctx.sort(keys)
+    inv, _, ms_out = ctx.check_sorted(out)
+    assert inv == 0 and ms_in == ms_out
+    assert int(out[0]) <= int(keys[: 1 << 24].min())
+    out2, _ = ctx.sort(keys)
+    assert torch.equal(out, out2)
+    del keys, out, out2
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("kind", ["uniform", "skewed", "lowzero", "midconst", "topbyte", "sorted",
                                   "extremes", "equal"])
