@@ -38,10 +38,6 @@ $(LIB)/libb200sort_prof.so: $(SRC)/*.cu $(HDRS)
 	for f in $(CU); do $(NVCC) $(NVFLAGS) -DB2S_PHASE_PROFILE -c $(SRC)/$$f.cu -o build/prof/$$f.o || exit 1; done
 	$(NVCC) $(ARCH) -shared -o $@ $(addprefix build/prof/,$(addsuffix .o,$(CU))) -lcudart
 
-# ablation experiments (timing only; output is wrong): make lbexp -> libb200sort_lb{LOOKBACK,RANK,WRITE}.so
-lbexp:
-	for w in 0; do mkdir -p build/lb$$w; for f in $(CU); do $(NVCC) $(NVFLAGS) -DB2S_MATCH_HYBRID=$$w -c $(SRC)/$$f.cu -o build/lb$$w/$$f.o || exit 1; done; $(NVCC) $(ARCH) -shared -o $(LIB)/libb200sort_lb$$w.so $(addprefix build/lb$$w/,$(addsuffix .o,$(CU))) -lcudart; done
-
 # one experimental build of one source: make variant NAME=x DEFS="-DFOO=1" [VSRC=merge_path]
 # -> lib/libb200sort_x.so (select with B2S_LIB)
 VSRC ?= radix_sort

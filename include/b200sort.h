@@ -198,6 +198,13 @@ b2s_status b2s_gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t 
 b2s_status b2s_check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
                             uint64_t* inversions, uint64_t* fingerprint, uint64_t* multiset,
                             uint32_t flags);
+/* cfg4a's skewed input (BASELINE.json configs[3](a): Zipf s=1.2 over 2^20
+ * values): key_i = the number of entries of the HOST table `thresholds`
+ * (nvalues ascending uint64, last = 2^53) that are <= (z_{first+i} >> 11),
+ * z = gen_data's stream for `seed`. Integer-only, so bit-identical to a host
+ * draw from the same table (oracle.zipf_thresholds / oracle.zipf_keys). */
+b2s_status b2s_gen_zipf(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
+                        const uint64_t* thresholds, uint32_t nvalues, void* out, uint32_t flags);
 
 #ifdef __cplusplus
 }

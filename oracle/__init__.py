@@ -154,6 +154,70 @@ def fingerprint(x: np.ndarray) -> int:
         return int(np.sum(_mix(w ^ _mix(idx)), dtype=np.uint64))
 
 
+def fingerprint_chunked(x: np.ndarray, first: int = 0, chunk: int = 1 << 25) -> int:
+    """fingerprint() of x computed in chunks (2^31-key outputs), x occupying
+    positions first.. of the sequence."""
+    total = np.uint64(0)
+    with np.errstate(over="ignore"):
+        for a in range(0, x.size, chunk):
+            part = x[a: a + chunk]
+            if part.dtype in (np.int32, np.int64):
+                w = part.astype(np.int64).view(np.uint64)
+            else:
+                w = part.astype(np.uint64)
+            idx = np.arange(first + a + 1, first + a + 1 + w.size, dtype=np.uint64)
+            total = total + np.sum(_mix(w ^ _mix(idx)), dtype=np.uint64)
+    return int(total)
+
+
+def multiset_hash(x: np.ndarray, chunk: int = 1 << 25) -> int:
+    """Order-independent sum_i mix(w_i) (b2s_check_sorted's multiset hash)."""
+    total = np.uint64(0)
+    with np.errstate(over="ignore"):
+        for a in range(0, x.size, chunk):
+            part = x[a: a + chunk]
+            w = part.astype(np.int64).view(np.uint64) if part.dtype in (np.int32, np.int64) \
+                else part.astype(np.uint64)
+            total = total + np.sum(_mix(w), dtype=np.uint64)
+    return int(total)
+
+
+def gen_keys(n: int, seed: int, dtype, shift: int = 0, chunk: int = 1 << 25) -> np.ndarray:
+    """(T)(z_i >> shift) over gen_data's stream (P/src/bench.cpp:57-71), the
+    BASELINE configs' inputs (cfg2: u32 >> 32, cfg3: i32 >> 33, cfg5: u64),
+    generated in chunks."""
+    out = np.empty(n, dtype=dtype)
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        z = gen_data_np(m, seed, first=a) >> np.uint64(shift)
+        out[a: a + m] = z.astype(dtype) if np.dtype(dtype).itemsize == 4 else z.view(dtype)
+    return out
+
+
+def zipf_thresholds(values: int = 1 << 20, s: float = 1.2) -> np.ndarray:
+    """Integer inverse-CDF table of Zipf(s) over `values` ranks (SURVEY.md
+    8(d), cfg4a): T[r] = floor(CDF(r) * 2^53) with the weights (r+1)^-s summed
+    in rank order in float64; T[-1] = 2^53. Rank r is drawn for
+    u = z >> 11 (53 bits) when T[r-1] <= u < T[r], so the draw itself is
+    integer arithmetic and bit-identical wherever the table is the same."""
+    w = np.power(np.arange(1, values + 1, dtype=np.float64), -s)
+    cdf = np.cumsum(w)
+    t = np.floor(cdf / cdf[-1] * float(1 << 53)).astype(np.uint64)
+    t[-1] = np.uint64(1 << 53)
+    return t
+
+
+def zipf_keys(n: int, seed: int, thresholds: np.ndarray, dtype=np.int32,
+              chunk: int = 1 << 25) -> np.ndarray:
+    """key_i = min r with (z_i >> 11) < T[r] (the rank is the key)."""
+    out = np.empty(n, dtype=dtype)
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        u = gen_data_np(m, seed, first=a) >> np.uint64(11)
+        out[a: a + m] = np.searchsorted(thresholds, u, side="right").astype(dtype)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # port (C restatement) wrappers
 

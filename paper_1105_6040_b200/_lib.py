@@ -23,7 +23,7 @@ EXPORTS = [
     "b2s_merge", "b2s_sort_batch", "b2s_partitioned_sort", "b2s_odd_even_sort", "b2s_plan_partition",
     "b2s_merge_split_padded",
     "b2s_sample_regular", "b2s_select_splitters", "b2s_bucket_bounds", "b2s_gen_keys",
-    "b2s_check_sorted", "b2s_exchange_buffer", "b2s_open_peer", "b2s_close_peers",
+    "b2s_check_sorted", "b2s_gen_zipf", "b2s_exchange_buffer", "b2s_open_peer", "b2s_close_peers",
 ]
 
 
@@ -74,6 +74,7 @@ _SIGS = {
     "b2s_bucket_bounds": (_st, [_p, _i, _p, _u64, _i, _p, _i, _p]),
     "b2s_gen_keys": (_st, [_p, _i, _u64, _u64, _u64, _i, _p, _u32]),
     "b2s_check_sorted": (_st, [_p, _i, _p, _u64, _p, _p, _p, _u32]),
+    "b2s_gen_zipf": (_st, [_p, _i, _u64, _u64, _u64, _p, _u32, _p, _u32]),
     "b2s_exchange_buffer": (_st, [_p, _u64, ctypes.POINTER(_p), _p]),
     "b2s_open_peer": (_st, [_p, _p, ctypes.POINTER(_p)]),
     "b2s_close_peers": (_st, [_p]),

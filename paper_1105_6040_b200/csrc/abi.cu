@@ -158,9 +158,17 @@ unsigned long long b2s_kernel_launches(void) { return b2s::launch_count(); }
 b2s_status b2s_exchange_buffer(b2s_ctx* ctx, uint64_t bytes, void** ptr, void* handle64) {
     B2S_TRY(check_ctx(ctx));
     if (ptr == nullptr || handle64 == nullptr) return set_error(B2S_EINVAL, "null output");
-    // peers may still be reading the current buffer: reallocation waits for
-    // this context's stream (the caller orders the peers' reads before it)
-    if (bytes > ctx->xbuf.bytes) B2S_CUDA(cudaStreamSynchronize(ctx->stream));
+    // Peers may hold the current buffer open (cudaIpcOpenMemHandle) and
+    // freeing an exported allocation before its importers close it is
+    // undefined, so a buffer that must grow is retired, not freed: it lives
+    // until b2s_destroy. Growth is geometric, so retired memory stays below
+    // the live buffer's size.
+    if (bytes > ctx->xbuf.bytes && ctx->xbuf.ptr != nullptr) {
+        ctx->xbuf_retired.push_back(ctx->xbuf.ptr);
+        ctx->xbuf.ptr = nullptr;
+        bytes = std::max<uint64_t>(bytes, ctx->xbuf.bytes + ctx->xbuf.bytes / 2);
+        ctx->xbuf.bytes = 0;
+    }
     B2S_TRY(ctx->xbuf.ensure(bytes));
     if (ctx->xbuf_handle_ptr != ctx->xbuf.ptr) {
         cudaIpcMemHandle_t h;
@@ -261,7 +269,7 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
                       &ctx->lookback, &ctx->hist,      &ctx->plan,      &ctx->parts,
                       &ctx->misc,     &ctx->stage_in,  &ctx->stage_out, &ctx->stage_vin,
                       &ctx->stage_vout, &ctx->xbuf, &ctx->seg_lookback, &ctx->seg_hist,
-                      &ctx->seg_plan, &ctx->kmerge, &ctx->oe_keys};
+                      &ctx->seg_plan, &ctx->kmerge, &ctx->oe_keys, &ctx->zipf_table};
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->gstream) cudaStreamDestroy(ctx->gstream);
     if (ctx->g_in) cudaEventDestroy(ctx->g_in);
@@ -270,6 +278,8 @@ b2s_status b2s_destroy(b2s_ctx* ctx) {
     for (cudaEvent_t e : ctx->side_done) cudaEventDestroy(e);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     for (DevBuf* b : bufs) b->release();
+    for (void* p : ctx->xbuf_retired) cudaFree(p);
+    ctx->xbuf_retired.clear();
     ctx->host_misc.release();
     for (int i = 0; i < 40; ++i)
         if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
@@ -375,6 +385,13 @@ b2s_status b2s_sort_batch(b2s_ctx* ctx, b2s_dtype dtype, const void* const* keys
         return set_error(B2S_EINVAL, "vals_in and vals_out must both be set or both be NULL");
     if (count > 0 && (keys_in == nullptr || keys_out == nullptr))
         return set_error(B2S_EINVAL, "null batch arrays");
+    if (n >= (1ull << 40)) return set_error(B2S_EINVAL, "n = %llu exceeds 2^40", (unsigned long long)n);
+    for (int i = 0; i < count && n > 0; ++i) {
+        if (keys_in[i] == nullptr || keys_out[i] == nullptr)
+            return set_error(B2S_EINVAL, "null key buffer in batch entry %d", i);
+        if (vals_in != nullptr && (vals_in[i] == nullptr || vals_out[i] == nullptr))
+            return set_error(B2S_EINVAL, "null payload buffer in batch entry %d", i);
+    }
     timing_reset(ctx);
     if (count == 0 || n == 0) return B2S_OK;
     const bool with_vals = vals_in != nullptr;
@@ -661,7 +678,7 @@ b2s_status partitioned_sort_dev(b2s_ctx* ctx, b2s_dtype dtype, const void* din, 
     const bool conc = !ctx->timing && p > 1;
     const int nside = std::min(p, kSideStreams);
     std::vector<size_t> lb_off(p + 1, 0);
-    for (int r = 0; r < p; ++r) lb_off[r + 1] = lb_off[r] + (2 * lookback_region_bytes(sizes[r]) + 16 + 255) / 256 * 256;
+    for (int r = 0; r < p; ++r) lb_off[r + 1] = lb_off[r] + (2 * lookback_region_bytes(sizes[r], (int)ksz, dvin != nullptr) + 16 + 255) / 256 * 256;
     if (conc) {
         B2S_TRY(ctx->seg_lookback.ensure(lb_off[p]));
         B2S_TRY(ctx->seg_hist.ensure((size_t)p * sizeof(RadixCounters)));
@@ -850,6 +867,21 @@ b2s_status b2s_gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t 
         return d2h_sync(ctx, out, ctx->stage_out.ptr, bytes);
     }
     return gen_keys(ctx, dtype, first, n, seed, shift, out);
+}
+
+b2s_status b2s_gen_zipf(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
+                        const uint64_t* thresholds, uint32_t nvalues, void* out, uint32_t flags) {
+    B2S_TRY(check_ctx(ctx));
+    if (!dtype_ok(dtype)) return set_error(B2S_EINVAL, "unknown dtype %d", (int)dtype);
+    if (nvalues < 1 || thresholds == nullptr) return set_error(B2S_EINVAL, "empty threshold table");
+    if (n > 0 && out == nullptr) return set_error(B2S_EINVAL, "null output");
+    if (flags & B2S_HOST) {
+        const size_t bytes = n * (size_t)key_bytes(dtype);
+        B2S_TRY(ctx->stage_out.ensure(bytes));
+        B2S_TRY(gen_zipf(ctx, dtype, first, n, seed, thresholds, nvalues, ctx->stage_out.ptr));
+        return d2h_sync(ctx, out, ctx->stage_out.ptr, bytes);
+    }
+    return gen_zipf(ctx, dtype, first, n, seed, thresholds, nvalues, out);
 }
 
 b2s_status b2s_check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,

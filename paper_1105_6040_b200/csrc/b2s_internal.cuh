@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -30,10 +31,22 @@ void clear_error();
     } while (0)
 
 // One-time setup per device: kernel attributes (opt-in shared memory) are set
-// per device, so a process driving several GPUs sets them on each.
-inline bool first_on_device(std::atomic<unsigned long long>& mask, int device) {
+// per device, so a process driving several GPUs sets them on each. The setup
+// runs under a mutex and the device counts as done only once it succeeded, so
+// no thread launches before the attributes are set and a failure is retried.
+struct DeviceOnce {
+    std::mutex m;
+    std::atomic<unsigned long long> done{0};
+};
+template <typename F>
+b2s_status once_per_device(DeviceOnce& o, int device, F&& setup) {
     const unsigned long long bit = 1ull << (device & 63);
-    return (mask.fetch_or(bit) & bit) == 0;
+    if (o.done.load(std::memory_order_acquire) & bit) return B2S_OK;
+    std::lock_guard<std::mutex> g(o.m);
+    if (o.done.load(std::memory_order_relaxed) & bit) return B2S_OK;
+    const b2s_status st = setup();
+    if (st == B2S_OK) o.done.fetch_or(bit, std::memory_order_release);
+    return st;
 }
 
 // every kernel launch of the library is counted (b2s_kernel_launches)
@@ -135,12 +148,14 @@ struct b2s_ctx {
     b2s::DevBuf xbuf;
     void* xbuf_handle_ptr = nullptr;  // allocation the cached handle belongs to
     unsigned char xbuf_handle[64] = {};
+    std::vector<void*> xbuf_retired;  // outgrown exported buffers (peers may map them)
     std::map<std::string, void*> peers;  // IPC handle bytes -> mapped pointer
     // partitioned sort: per-partition scratch and side streams for the
     // concurrent local sorts
     b2s::DevBuf seg_lookback, seg_hist, seg_plan;
     b2s::DevBuf kmerge;  // grouped k-way merge: samples, tags, cuts
     b2s::DevBuf oe_keys;  // odd-even sort: two slots of width ceil(n/p) per block
+    b2s::DevBuf zipf_table;  // b2s_gen_zipf's threshold table
     std::vector<cudaStream_t> side;
     std::vector<cudaEvent_t> side_done;
     cudaEvent_t fork = nullptr;
@@ -184,11 +199,11 @@ void timing_reset(b2s_ctx* ctx);
 struct SortScratch {
     void* alt_keys;          // n keys: ping-pong partner
     uint32_t* alt_vals;      // n payload words (or null)
-    void* lookback;          // 2 * lookback_region_bytes(n) + 16
+    void* lookback;          // 2 * lookback_region_bytes(n, ...) + 16
     RadixCounters* ctr;
     RadixPlan* plan;
 };
-size_t lookback_region_bytes(uint64_t n);
+size_t lookback_region_bytes(uint64_t n, int kbytes, bool vals);  // one region, for the tile actually launched
 constexpr int kSideStreams = 8;  // concurrent partition sorts
 
 // device entry points implemented in the .cu files (all async on ctx->stream)
@@ -214,6 +229,8 @@ b2s_status gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, u
                     int shift, void* out);
 b2s_status check_sorted(b2s_ctx* ctx, b2s_dtype dtype, const void* keys, uint64_t n,
                         uint64_t* inv, uint64_t* fp, uint64_t* ms);
+b2s_status gen_zipf(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
+                    const uint64_t* thresholds, uint32_t nvalues, void* out);
 
 // ---------------------------------------------------------------------------
 // device helpers

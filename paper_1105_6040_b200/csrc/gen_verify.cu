@@ -27,6 +27,26 @@ __global__ void gen_keys_kernel(uint64_t first, uint64_t n, uint64_t seed, int s
     }
 }
 
+// cfg4a's Zipf stream: u = z_i >> 11 (53 bits) of
+// gen_data's element i, key = number of thresholds <= u (the rank drawn by the
+// integer inverse-CDF table, see oracle.zipf_thresholds). Integer only, so the
+// device and the host draw identical keys from the same table.
+template <typename T>
+__global__ void gen_zipf_kernel(uint64_t first, uint64_t n, uint64_t seed,
+                                const uint64_t* __restrict__ t, uint32_t nv, T* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t u = mix64(seed + (first + i + 1) * kGamma) >> 11;
+        uint32_t lo = 0, hi = nv;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(t + mid) <= u) lo = mid + 1;
+            else hi = mid;
+        }
+        out[i] = (T)lo;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ uint64_t widen(T x) {
     return (uint64_t)(int64_t)x;  // sign-extends signed types, zero-extends unsigned
@@ -85,6 +105,37 @@ b2s_status gen_keys(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, u
             break;
     }
     B2S_LAUNCHED();
+    return B2S_OK;
+}
+
+b2s_status gen_zipf(b2s_ctx* ctx, b2s_dtype dtype, uint64_t first, uint64_t n, uint64_t seed,
+                    const uint64_t* thresholds, uint32_t nvalues, void* out) {
+    if (n == 0) return B2S_OK;
+    B2S_TRY(ctx->zipf_table.ensure((size_t)nvalues * 8));
+    uint64_t* t = static_cast<uint64_t*>(ctx->zipf_table.ptr);
+    B2S_CUDA(cudaMemcpyAsync(t, thresholds, (size_t)nvalues * 8, cudaMemcpyHostToDevice, ctx->stream));
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+    switch (dtype) {
+        case B2S_I32:
+            gen_zipf_kernel<int32_t><<<grid, 256, 0, ctx->stream>>>(first, n, seed, t, nvalues,
+                                                                    static_cast<int32_t*>(out));
+            break;
+        case B2S_U32:
+            gen_zipf_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(first, n, seed, t, nvalues,
+                                                                     static_cast<uint32_t*>(out));
+            break;
+        case B2S_I64:
+            gen_zipf_kernel<int64_t><<<grid, 256, 0, ctx->stream>>>(first, n, seed, t, nvalues,
+                                                                    static_cast<int64_t*>(out));
+            break;
+        case B2S_U64:
+            gen_zipf_kernel<unsigned long long><<<grid, 256, 0, ctx->stream>>>(
+                first, n, seed, t, nvalues, static_cast<unsigned long long*>(out));
+            break;
+    }
+    B2S_LAUNCHED();
+    // the table is pageable host memory: the copy is staged before the call
+    // returns, so the caller may free it
     return B2S_OK;
 }
 

@@ -538,10 +538,12 @@ template <typename T, bool VALS>
 b2s_status launch_groups(b2s_ctx* ctx, const KRuns<T>& R, const uint64_t* cuts, uint64_t ngroups,
                          T* out, uint32_t* vout) {
     auto kern = kmerge_group_kernel<T, VALS>;
-    static std::atomic<unsigned long long> set_on{0};
-    if (first_on_device(set_on, ctx->device))
+    static DeviceOnce once;
+    B2S_TRY(once_per_device(once, ctx->device, [&]() -> b2s_status {
         B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)group_smem<T, VALS>(group_cap<T, VALS>(kMaxK))));
+        return B2S_OK;
+    }));
     const uint32_t cap = group_cap<T, VALS>(R.k);
     kern<<<(unsigned)ngroups, kKThreads, group_smem<T, VALS>(cap), ctx->stream>>>(R, cuts, cap, out, vout);
     B2S_LAUNCHED();

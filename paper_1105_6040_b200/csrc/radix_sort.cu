@@ -31,8 +31,6 @@
 //
 // HBM traffic per executed pass: read + write of every key (and payload):
 // 2 * (key_bytes + val_bytes) * n. The prologue reads key_bytes * n once.
-#include <cub/warp/warp_scan.cuh>
-
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -679,9 +677,6 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
                                             : i;
             const U k = kbuf[si];
             const OFF g = gbase[digit_of(k, shift, dxor)] + (OFF)i;
-#ifdef B2S_ABLATE_WRITE
-            if (k == (U)0x12345678 && g == 0)
-#endif
             // streaming (evict-first) stores, except for structured input,
             // whose runs land in few, long stretches (measured per 2^28-key
             // u32 pass: uniform 0.718 streaming vs 0.725 plain, ascending
@@ -693,7 +688,6 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
                 __stcs(dst + g, k);
                 if constexpr (VALS) __stcs(vdst + g, vbuf[sizeof(U) == 4 ? si : swz<4, SWZ>(i)]);
             }
-#ifndef B2S_ABLATE_NEXTHIST
             if (nd.on) {
                 const uint32_t dn = digit_of(k, nd.shift, nd.dxor);
                 if (AGG && full) {
@@ -707,13 +701,12 @@ __device__ __forceinline__ void writeout_tile(const U* kbuf, const uint32_t* vbu
                     atomicAdd(nd.hist + dn, 1u);  // ATOMS.POPC.INC
                 }
             }
-#endif
         }
     }
 }
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, bool FULL, bool FROM_SMEM,
-          bool PIPE, int RANK, bool SWZ = false, bool SEP = false, typename Claim, typename Between>
+          int RANK, bool SWZ = false, bool SEP = false, typename Claim, typename Between>
 __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Between& between,
                                               typename TileShared<LB>::OFF* gbase_out, uint32_t tile,
                                               uint32_t tile_valid, uint64_t tile_base,
@@ -734,7 +727,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // 16-bit counters) and ranking is one lookup of the warp's digit base --
     // for full TMA-landed tiles; other tiles rank as 1. 6 is 5 with 2's hot
     // digit (ranked by ballots in the early phase), other tiles rank as 2.
-    constexpr bool ER = (RANK == 5 || RANK == 6) && FULL && FROM_SMEM && !PIPE;
+    constexpr bool ER = (RANK == 5 || RANK == 6) && FULL && FROM_SMEM;
     constexpr int RB = RANK == 5 ? 1 : (RANK == 6 ? 2 : RANK);  // non-ER behaviour
     // ELB (experiment, off): the look-back runs right after the digit section
     // (its warps rank afterwards), so inclusive prefixes are published
@@ -802,7 +795,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // place), so no other warp's data shares their words
     constexpr bool ECNT = ER && B2S_ECNT_IN_CNT;
     uint32_t* ecnt = ECNT ? s_cnt + warp * HALF : s_early + warp * kRadix;
-    if constexpr (!PIPE) {
+    {
         // each warp clears its own counters: 512 B of s_cnt (RANK 5/6, packed
         // pairs) or 1 KB of the idle tile buffer (nothing streams into it
         // before this tile's look-back is done)
@@ -874,7 +867,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             if (FULL || wbase + j * 32 + lane < tile_valid) atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
         }
     }
-    if constexpr (!PIPE) between();  // regular kernel: publish the next tile id
+    between();  // publish the next tile id
     __syncthreads();  // also: every warp has read its keys out of kbuf
     B2S_PHASE(1);
     // With the early counts in s_cnt the other tile buffer holds nothing but
@@ -962,11 +955,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         if (tid < kRadix) {
             unsigned long long excl = 0;
             const uint32_t mycount = (tid + 1 < kRadix ? sh.start[tid + 1] : (uint32_t)tile_valid) - sh.start[tid];
-    #ifdef B2S_ABLATE_LOOKBACK
-            if (false) {
-    #else
             if (tile > 0) {
-    #endif
                 int64_t pred = (int64_t)tile - 1;
                 bool done = false;
                 const LB* col = lb_cur + tid;
@@ -1125,9 +1114,6 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     for (int j = 0; j < ITEMS; ++j) {
         const bool valid = FULL || (wbase + j * 32 + lane < tile_valid);
         const uint32_t d = valid ? digit_of(keys[j], shift, dxor) : (uint32_t)kRadix;
-#ifdef B2S_ABLATE_RANK
-        const uint32_t peers = 1u << lane;
-#else
         uint32_t r;
         if constexpr (RB >= 1) {
             // lane-ordered shared atomics: lanes adding to the same counter in one
@@ -1148,7 +1134,6 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         } else {
             peers = match_digit<FULL ? 8 : 9>(d);
         }
-#endif
         const uint32_t below = __popc(peers & lanemask_lt);
         const int leader = 31 - __clz(peers);
         const uint32_t sh16 = 16 * (d & 1);
@@ -1161,26 +1146,14 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         const uint32_t base = (__shfl_sync(0xffffffffu, old, leader) >> sh16) & 0xFFFFu;
         r = base + below;
         }
-#ifdef B2S_ABLATE_SCATTER
-        if (valid && r == 0x7fffffff) {
-#else
         if (valid) {
-#endif
             sts_key(keys_a + swz<sizeof(U), SWZ>(r) * (uint32_t)sizeof(U), keys[j]);
             if constexpr (VALS) sts_key(vals_a + 4 * swz<4, SWZ>(r), vals[j]);
         }
     }
     B2S_PHASE(3);
-    if constexpr (PIPE) {
-        // this warp is done with its counters: clear them for the next tile,
-        // then write out the previous tile while the look-back reads land
-#pragma unroll
-        for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
-        between();
-    }
 
     if constexpr (!ELB) lookback();
-    if constexpr (PIPE) return;  // the caller syncs; this tile is written next round
     __syncthreads();
     B2S_PHASE(4);
     if constexpr (!EARLY_CLAIM) claim_next();
@@ -1379,16 +1352,16 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 mbar_wait(mbar_a[lb_], (parity >> lb_) & 1u);
                 parity ^= 1u << lb_;
                 B2S_PHASE(0);
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, false, TR, SWZ, SEP>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, TR, SWZ, SEP>(
                     claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
             } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, false, TR, SWZ, SEP>(
+                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, TR, SWZ, SEP>(
                     claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
                     s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
             }
         } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, false, TR, SWZ, SEP>(
+            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, TR, SWZ, SEP>(
                 claim, publish, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
                 nd, s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
         }
@@ -1418,521 +1391,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
 }
 
-// Software-pipelined variant: tile k is ranked while tile k-1 (ranked in
-// the previous round) is written out, and tile k's look-back runs after that
-// write-out -- by then its prefetched predecessor window has landed and most
-// predecessors have posted inclusive prefixes, so the look-back rarely waits.
-// Three tile buffers rotate: k+1 landing by TMA, k being ranked in place,
-// k-1 being written out.
-template <typename U, bool VALS, int THREADS, int ITEMS>
-struct PipeSmem {
-    static constexpr int WARPS = THREADS / 32;
-    static constexpr int TILE = THREADS * ITEMS;
-    static constexpr size_t kCnt = (size_t)WARPS * (kRadix / 2) * 4;
-    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);
-    static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
-    static constexpr size_t kMatch = MATCH_SMEM ? (size_t)WARPS * kRadix * 4 : 0;
-    static constexpr size_t kEarly = MATCH_SMEM ? 0 : (size_t)WARPS * kRadix * 4;
-    static constexpr size_t bytes = kCnt + 3 * kKeys + 3 * kVals + kMatch + kEarly;
-};
-
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
-__global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan* __restrict__ plan,
-                                                                      RadixCounters* __restrict__ ctr,
-                                                                      int slot, uint64_t n,
-                                                                      uint32_t ntiles,
-                                                                      LB* __restrict__ lb_cur,
-                                                                      LB* __restrict__ lb_next) {
-    using SM = PipeSmem<U, VALS, THREADS, ITEMS>;
-    constexpr int TILE = SM::TILE;
-    static_assert(THREADS >= kRadix, "one thread per digit is required");
-    static_assert(TILE < 65536, "packed 16-bit warp counters");
-
-    const int na = plan->num_active;
-    if (slot >= na) return;
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem);
-    U* kbuf[3];
-    uint32_t* vbuf[3];
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-        kbuf[b] = reinterpret_cast<U*>(smem + SM::kCnt + b * SM::kKeys);
-        vbuf[b] = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 3 * SM::kKeys + b * SM::kVals);
-    }
-    uint32_t* s_match = reinterpret_cast<uint32_t*>(smem + SM::kCnt + 3 * SM::kKeys + 3 * SM::kVals);
-    uint32_t* s_early = MATCH_SMEM ? s_match : s_match + SM::kMatch / 4;
-    __shared__ TileShared<LB> sh;
-    __shared__ typename TileShared<LB>::OFF s_gbase2[2][kRadix];
-    __shared__ alignas(8) unsigned long long s_mbar3[3];
-    __shared__ uint32_t s_tile3[3];
-
-    const int tid = threadIdx.x;
-    const int shift = 8 * plan->digit[slot];
-    const uint32_t dxor = plan->dxor[slot];
-    const U* src = static_cast<const U*>(plan->ksrc[slot]);
-    U* dst = static_cast<U*>(plan->kdst[slot]);
-    const uint32_t* vsrc = plan->vsrc[slot];
-    uint32_t* vdst = plan->vdst[slot];
-    NextDigit nd;
-    nd.on = slot + 1 < na && !plan->all_hist;
-    nd.shift = nd.on ? 8 * plan->digit[slot + 1] : 0;
-    nd.dxor = nd.on ? plan->dxor[slot + 1] : 0u;
-    nd.hist = sh.nhist;
-    const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
-                     (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
-    const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
-
-    auto prefetch = [&](uint32_t t, int b) {  // one thread only
-        if (tma && t < ntiles && n - (uint64_t)t * TILE >= (uint64_t)TILE) {
-            const uint32_t mb = smem_addr(&s_mbar3[b]);
-            fence_proxy_async();
-            mbar_expect_tx(mb, tx_bytes);
-            bulk_g2s(smem_addr(kbuf[b]), src + (uint64_t)t * TILE, (uint32_t)SM::kKeys, mb);
-            if constexpr (VALS)
-                bulk_g2s(smem_addr(vbuf[b]), vsrc + (uint64_t)t * TILE, (uint32_t)SM::kVals, mb);
-        }
-    };
-
-    if (tid < kRadix) {
-        const unsigned long long c = plan->hist[slot][tid];
-        unsigned long long incl = c;
-        const int lane = tid & 31;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) sh.wsum64[tid >> 5] = incl;
-        sh.goff[tid] = (typename TileShared<LB>::OFF)(incl - c);
-        sh.nhist[tid] = 0;
-    }
-    for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
-    for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_early[i] = 0;
-    if constexpr (MATCH_SMEM)
-        for (int i = tid; i < SM::WARPS * kRadix; i += THREADS) s_match[i] = 0;
-    if (tid == THREADS - 1) {
-        for (int b = 0; b < 3; ++b) mbar_init(smem_addr(&s_mbar3[b]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-        s_tile3[0] = t;
-        prefetch(t, 0);
-    }
-    __syncthreads();
-    if (tid < kRadix) {
-        unsigned long long base = 0;
-#pragma unroll
-        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? sh.wsum64[w] : 0ull;
-        sh.goff[tid] += (typename TileShared<LB>::OFF)base;
-    }
-
-    int cur = 0;           // buffer of the current tile (ring of 3)
-    int prev = -1;         // buffer of the staged previous tile, -1 if none
-    uint32_t prev_valid = 0;
-    int gcur = 0;          // gbase slot of the current tile (ring of 2)
-    uint32_t parity = 0;   // bit b: phase parity of buffer b's mbarrier
-    unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long prof_t = clock64();
-    (void)prof_t;
-    for (;;) {
-        const uint32_t tile = s_tile3[cur];
-        if (tile >= ntiles) break;
-        const int nxt = cur == 2 ? 0 : cur + 1;
-        if (tid == THREADS - 1) {  // claim tile k+1 into the buffer tile k-2 freed
-            const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-            s_tile3[nxt] = t;
-            prefetch(t, nxt);
-        }
-        const uint64_t tile_base = (uint64_t)tile * TILE;
-        const uint64_t rem = n - tile_base;
-        if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
-        const int pb = prev;
-        const uint32_t pv = prev_valid;
-        const int pg = gcur ^ 1;
-        auto write_prev = [&]() {
-            if (pb >= 0)
-                writeout_tile<U, VALS, LB, THREADS, ITEMS>(kbuf[pb], vbuf[pb], s_gbase2[pg], pv, dst,
-                                                           vdst, shift, dxor, nd);
-        };
-        auto noop = []() {};
-        if (rem >= (uint64_t)TILE) {
-            if (tma) {
-                mbar_wait(smem_addr(&s_mbar3[cur]), (parity >> cur) & 1u);
-                parity ^= 1u << cur;
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, true, RANK>(
-                    noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
-                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
-                    prof_t);
-            } else {
-                onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, true, RANK>(
-                    noop, write_prev, s_gbase2[gcur], tile, TILE, tile_base, src, dst, vsrc, vdst,
-                    lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
-                    prof_t);
-            }
-            prev_valid = TILE;
-        } else {
-            onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, true, RANK>(
-                noop, write_prev, s_gbase2[gcur], tile, (uint32_t)rem, tile_base, src, dst, vsrc,
-                vdst, lb_cur, shift, dxor, nd, s_cnt, kbuf[cur], vbuf[cur], kbuf[cur], vbuf[cur], s_match, s_early, sh, prof_acc,
-                prof_t);
-            prev_valid = (uint32_t)rem;
-        }
-        __syncthreads();
-        prev = cur;
-        gcur ^= 1;
-        cur = nxt;
-    }
-    if (prev >= 0)
-        writeout_tile<U, VALS, LB, THREADS, ITEMS>(kbuf[prev], vbuf[prev], s_gbase2[gcur ^ 1],
-                                                   prev_valid, dst, vdst, shift, dxor, nd);
-    __syncthreads();
-    if (nd.on && tid < kRadix && sh.nhist[tid])
-        atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
-}
-
-// ---------------------------------------------------------------------------
-// Warp-specialised onesweep: warps 0-7 ("rankers") load, count, publish and
-// rank tile k while warps 8-15 ("writers") resolve tile k-1's look-back and
-// write it out, then refill its buffer with a TMA copy of a new tile. Three
-// tile buffers rotate; the groups hand tiles over with mbarriers and sync
-// internally with named barriers, so the look-back latency and the write-out
-// of one tile overlap the ranking of the next.
-
-__device__ __forceinline__ void named_bar(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-
-constexpr int kWsSlots = 3;
-constexpr uint32_t kWsEnd = 0xFFFFFFFFu;
-
-template <typename U, bool VALS, int ITEMS>
-struct WsSmem {
-    static constexpr int TILE = 256 * ITEMS;  // ranked by 256 threads
-    static constexpr size_t kKeys = (size_t)TILE * sizeof(U);
-    static constexpr size_t kVals = VALS ? (size_t)TILE * 4 : 0;
-    static constexpr size_t kCnt = 8 * (kRadix / 2) * 4;   // rankers' packed counters
-    static constexpr size_t kEarly = 8 * kRadix * 4;       // rankers' early counts
-    static constexpr size_t bytes = kWsSlots * (kKeys + kVals) + kCnt + kEarly;
-};
-
-template <typename LB>
-struct WsShared {
-    using OFF = LB;
-    OFF goff[kRadix];
-    OFF gbase[kRadix];             // writers only
-    uint32_t start[2][kRadix];     // per tile parity: digit starts in the tile
-    uint32_t nhist[kRadix];
-    uint32_t wsum[8];
-    unsigned long long wsum64[kRadix / 32];
-    uint32_t slot_tile[kWsSlots];
-    uint32_t slot_valid[kWsSlots];
-    uint32_t slot_tma[kWsSlots];
-    uint32_t staged_tile[2];
-    uint32_t staged_valid[2];
-    uint32_t dummy[32];
-    alignas(8) unsigned long long full[kWsSlots];  // slot landed / set (writer -> ranker)
-    alignas(8) unsigned long long staged[2];       // tile ranked + staged (ranker -> writer)
-    alignas(8) unsigned long long statefree[2];    // start[] of a parity free (writer -> ranker)
-};
-
-template <typename U, bool VALS, typename LB, int ITEMS>
-__global__ void __launch_bounds__(512, 2) onesweep_ws_kernel(RadixPlan* __restrict__ plan,
-                                                             RadixCounters* __restrict__ ctr,
-                                                             int slot, uint64_t n, uint32_t ntiles,
-                                                             LB* __restrict__ lb_cur,
-                                                             LB* __restrict__ lb_next) {
-    using SM = WsSmem<U, VALS, ITEMS>;
-    using W = LookbackWord<LB>;
-    using OFF = LB;
-    constexpr int TILE = SM::TILE;
-    constexpr int HALF = kRadix / 2;
-    constexpr int WSEG = 32 * ITEMS;
-    static_assert(TILE < 65536, "packed 16-bit warp counters");
-
-    const int na = plan->num_active;
-    if (slot >= na) return;
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    U* kbuf[kWsSlots];
-    uint32_t* vbuf[kWsSlots];
-#pragma unroll
-    for (int b = 0; b < kWsSlots; ++b) {
-        kbuf[b] = reinterpret_cast<U*>(smem + b * SM::kKeys);
-        vbuf[b] = reinterpret_cast<uint32_t*>(smem + kWsSlots * SM::kKeys + b * SM::kVals);
-    }
-    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + kWsSlots * (SM::kKeys + SM::kVals));
-    uint32_t* s_early = s_cnt + SM::kCnt / 4;
-    __shared__ WsShared<LB> sh;
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    const bool ranker = warp < 8;
-    const int shift = 8 * plan->digit[slot];
-    const uint32_t dxor = plan->dxor[slot];
-    const U* src = static_cast<const U*>(plan->ksrc[slot]);
-    U* dst = static_cast<U*>(plan->kdst[slot]);
-    const uint32_t* vsrc = plan->vsrc[slot];
-    uint32_t* vdst = plan->vdst[slot];
-    const bool nd_on = slot + 1 < na && !plan->all_hist;
-    const int nd_shift = nd_on ? 8 * plan->digit[slot + 1] : 0;
-    const uint32_t nd_dxor = nd_on ? plan->dxor[slot + 1] : 0u;
-    const bool tma = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
-                     (!VALS || (reinterpret_cast<uintptr_t>(vsrc) & 15) == 0);
-    const uint32_t tx_bytes = (uint32_t)(SM::kKeys + SM::kVals);
-
-    // claim a tile into slot b and start its copy (one writer thread)
-    auto fill = [&](int b) {
-        const uint32_t t = atomicAdd(&plan->tile_counter[slot], 1u);
-        const uint32_t mb = smem_addr(&sh.full[b]);
-        if (t >= ntiles) {
-            sh.slot_tile[b] = kWsEnd;
-            mbar_arrive(mb);
-            return;
-        }
-        const uint64_t rem = n - (uint64_t)t * TILE;
-        const uint32_t valid = rem < (uint64_t)TILE ? (uint32_t)rem : (uint32_t)TILE;
-        sh.slot_tile[b] = t;
-        sh.slot_valid[b] = valid;
-        const bool use_tma = tma && valid == (uint32_t)TILE;
-        sh.slot_tma[b] = use_tma;
-        if (use_tma) {
-            fence_proxy_async();
-            mbar_expect_tx(mb, tx_bytes);
-            bulk_g2s(smem_addr(kbuf[b]), src + (uint64_t)t * TILE, (uint32_t)SM::kKeys, mb);
-            if constexpr (VALS)
-                bulk_g2s(smem_addr(vbuf[b]), vsrc + (uint64_t)t * TILE, (uint32_t)SM::kVals, mb);
-        } else {
-            mbar_arrive(mb);
-        }
-    };
-
-    // setup: digit offsets, counters, barriers, first fills
-    if (tid < kRadix) {
-        const unsigned long long c = plan->hist[slot][tid];
-        unsigned long long incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) sh.wsum64[tid >> 5] = incl;
-        sh.goff[tid] = (OFF)(incl - c);
-        sh.nhist[tid] = 0;
-    }
-    for (int i = tid; i < 8 * HALF; i += 512) s_cnt[i] = 0;
-    for (int i = tid; i < 8 * kRadix; i += 512) s_early[i] = 0;
-    if (tid == 0) {
-        for (int b = 0; b < kWsSlots; ++b) mbar_init(smem_addr(&sh.full[b]), 1);
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_addr(&sh.staged[b]), 1);
-            mbar_init(smem_addr(&sh.statefree[b]), 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (tid < kRadix) {
-        unsigned long long base = 0;
-#pragma unroll
-        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? sh.wsum64[w] : 0ull;
-        sh.goff[tid] += (OFF)base;
-    }
-    if (tid == 256)
-        for (int b = 0; b < kWsSlots; ++b) fill(b);
-    __syncthreads();
-
-    if (ranker) {
-        // ------------------------------------------------------------ rankers
-        const uint32_t cnt_a = smem_addr(s_cnt + warp * HALF);
-        uint32_t* ecnt = s_early + warp * kRadix;
-        const uint32_t dummy_a = smem_addr(sh.dummy + lane);
-        uint32_t ph_full = 0, ph_free = 0;
-        for (uint32_t k = 0;; ++k) {
-            const int s = (int)(k % kWsSlots);
-            const int b = (int)(k & 1);
-            mbar_wait(smem_addr(&sh.full[s]), (ph_full >> s) & 1u);
-            ph_full ^= 1u << s;
-            const uint32_t tile = sh.slot_tile[s];
-            if (tile == kWsEnd) {
-                if (tid == 0) {
-                    sh.staged_tile[b] = kWsEnd;
-                    mbar_arrive(smem_addr(&sh.staged[b]));
-                }
-                break;
-            }
-            if (k >= 2) {  // the writers are done with start[b] of tile k-2
-                mbar_wait(smem_addr(&sh.statefree[b]), (ph_free >> b) & 1u);
-                ph_free ^= 1u << b;
-            }
-            const uint32_t valid = sh.slot_valid[s];
-            const bool full = valid == (uint32_t)TILE;
-            const bool from_smem = sh.slot_tma[s] != 0;
-            const uint64_t tile_base = (uint64_t)tile * TILE;
-            if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
-            U* kb = kbuf[s];
-            uint32_t* vb = vbuf[s];
-            const uint32_t wbase = warp * WSEG;
-            U keys[ITEMS];
-            uint32_t vals[VALS ? ITEMS : 1];
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                const uint32_t idx = wbase + j * 32 + lane;
-                if (from_smem) {
-                    keys[j] = kb[idx];
-                    if constexpr (VALS) vals[j] = vb[idx];
-                } else {
-                    keys[j] = idx < valid ? src[tile_base + idx] : U(0);
-                    if constexpr (VALS) vals[j] = idx < valid ? vsrc[tile_base + idx] : 0u;
-                }
-            }
-            // early counts
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                const uint32_t d = digit_of(keys[j], shift, dxor);
-                if (full || wbase + j * 32 + lane < valid)
-                    atomicAdd(ecnt + ((d & 1) * HALF + (d >> 1)), 1u);
-            }
-            named_bar(1, 256);
-            // digit pairs: prefix over the 8 ranker warps, publish aggregates
-            uint32_t pair = 0;
-            if (tid < HALF) {
-#pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    uint32_t* e = s_early + w * kRadix;
-                    const uint32_t c = e[tid] | (e[HALF + tid] << 16);
-                    e[tid] = 0;
-                    e[HALF + tid] = 0;
-                    s_cnt[w * HALF + tid] = pair;
-                    pair += c;
-                }
-                const uint32_t c0 = pair & 0xFFFFu, c1 = pair >> 16;
-                LB* slotp = lb_cur + (size_t)tile * kRadix + 2 * tid;
-                const LB flag = tile == 0 ? W::kInc : W::kAgg;
-                st_relaxed(slotp, flag | (LB)c0);
-                st_relaxed(slotp + 1, flag | (LB)c1);
-                uint32_t incl = c0 + c1;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                if (lane == 31) sh.wsum[warp] = incl;
-                sh.start[b][2 * tid] = incl - c0 - c1;
-                sh.start[b][2 * tid + 1] = incl - c1;
-            }
-            named_bar(1, 256);
-            if (tid < HALF) {
-                uint32_t base = 0;
-#pragma unroll
-                for (int w = 0; w < HALF / 32; ++w) base += (w < warp) ? sh.wsum[w] : 0u;
-                const uint32_t s0 = sh.start[b][2 * tid] + base, s1 = sh.start[b][2 * tid + 1] + base;
-                sh.start[b][2 * tid] = s0;
-                sh.start[b][2 * tid + 1] = s1;
-                const uint32_t add = s0 | (s1 << 16);
-#pragma unroll
-                for (int w = 0; w < 8; ++w) s_cnt[w * HALF + tid] += add;
-            }
-            named_bar(1, 256);
-            // rank (lane-ordered atomics) and stage in place
-            const uint32_t keys_a = smem_addr(kb), vals_a = smem_addr(vb);
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                const bool ok = full || wbase + j * 32 + lane < valid;
-                const uint32_t d = digit_of(keys[j], shift, dxor);
-                const uint32_t s16 = 16 * (d & 1);
-                const uint32_t old = atom_add_shared(ok ? cnt_a + 4 * (d >> 1) : dummy_a,
-                                                     ok ? 1u << s16 : 0u);
-                const uint32_t r = (old >> s16) & 0xFFFFu;
-                if (ok) {
-                    sts_key(keys_a + r * (uint32_t)sizeof(U), keys[j]);
-                    if constexpr (VALS) sts_key(vals_a + 4 * r, vals[j]);
-                }
-            }
-#pragma unroll
-            for (int i = lane; i < HALF; i += 32) s_cnt[warp * HALF + i] = 0;
-            named_bar(1, 256);
-            if (tid == 0) {
-                sh.staged_tile[b] = tile;
-                sh.staged_valid[b] = valid;
-                mbar_arrive(smem_addr(&sh.staged[b]));
-            }
-        }
-    } else {
-        // ------------------------------------------------------------ writers
-        const int wt = tid - 256;  // 0..255: one digit each for the look-back
-        uint32_t ph_staged = 0;
-        for (uint32_t k = 0;; ++k) {
-            const int s = (int)(k % kWsSlots);
-            const int b = (int)(k & 1);
-            mbar_wait(smem_addr(&sh.staged[b]), (ph_staged >> b) & 1u);
-            ph_staged ^= 1u << b;
-            const uint32_t tile = sh.staged_tile[b];
-            if (tile == kWsEnd) break;
-            const uint32_t valid = sh.staged_valid[b];
-            // look-back for digit wt
-            {
-                const uint32_t st0 = sh.start[b][wt];
-                const uint32_t mycount = (wt + 1 < kRadix ? sh.start[b][wt + 1] : valid) - st0;
-                unsigned long long excl = 0;
-                if (tile > 0) {
-                    int64_t pred = (int64_t)tile - 1;
-                    bool done = false;
-                    const LB* col = lb_cur + wt;
-                    LB* mine = lb_cur + (size_t)tile * kRadix + wt;
-                    while (__any_sync(0xffffffffu, !done)) {
-                        if (!done) {
-                            LB w[4];
-#pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * kRadix) : W::kInc;
-                            bool stop = false;
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const LB f = W::flag(w[i]);
-                                if (!stop && f != 0) {
-                                    excl += (unsigned long long)(w[i] & W::kMask);
-                                    done = (f == 2);
-                                    stop = done;
-                                    pred -= done ? 0 : 1;
-                                } else {
-                                    stop = true;
-                                }
-                            }
-                            if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
-                        }
-                    }
-                }
-                sh.gbase[wt] = (OFF)(sh.goff[wt] + excl - st0);
-            }
-            named_bar(2, 256);
-            if (wt == 0) mbar_arrive(smem_addr(&sh.statefree[b]));  // start[b] no longer read
-            // write out the staged tile from slot s
-            const U* kb = kbuf[s];
-            const uint32_t* vb = vbuf[s];
-            const bool full = valid == (uint32_t)TILE;
-#pragma unroll 4
-            for (int j = 0; j < ITEMS; ++j) {
-                const uint32_t i = j * 256 + wt;
-                if (full || i < valid) {
-                    const U key = kb[i];
-                    const OFF g = sh.gbase[digit_of(key, shift, dxor)] + (OFF)i;
-                    __stcs(dst + g, key);
-                    if constexpr (VALS) __stcs(vdst + g, vb[i]);
-                    if (nd_on) atomicAdd(sh.nhist + digit_of(key, nd_shift, nd_dxor), 1u);
-                }
-            }
-            named_bar(2, 256);
-            if (wt == 0) fill(s);  // slot s is free: claim the next tile into it
-        }
-        named_bar(2, 256);
-        if (nd_on && wt < kRadix && sh.nhist[wt])
-            atomicAdd(&ctr->hist[slot + 1][wt], (unsigned long long)sh.nhist[wt]);
-    }
-}
-
 template <typename U>
 __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n, int with_vals) {
     if (!plan->do_copy) return;
@@ -1948,12 +1406,6 @@ __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n
     }
 }
 
-// Tile configurations. Registers must stay <= 65536 / (THREADS * MINB) so
-// MINB CTAs are resident per SM; B2S_ONESWEEP_CFG selects one for tuning runs.
-struct TileCfg {
-    int threads, items;
-};
-
 // B2S_ALL_HIST: 1 (default) all-digit prologue for 4-byte keys, 2 also for
 // 8-byte keys, 0 never (each next digit is counted inside the passes)
 int all_hist_mode() {
@@ -1963,15 +1415,6 @@ int all_hist_mode() {
         v = e ? atoi(e) : 1;
     }
     return v;
-}
-
-int onesweep_cfg() {
-    static int cfg = -1;
-    if (cfg < 0) {
-        const char* e = getenv("B2S_ONESWEEP_CFG");
-        cfg = e ? atoi(e) : 0;
-    }
-    return cfg;
 }
 
 // A pass is skewed when one digit holds more than n >> B2S_SKEW_SHIFT keys
@@ -2003,8 +1446,8 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
                           onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 3>,
                           onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 4>};
     static int occ[3] = {-1, -1, -1};  // per instantiation (one device type)
-    static std::atomic<unsigned long long> set_on{0};
-    if (first_on_device(set_on, ctx->device)) {
+    static DeviceOnce once;
+    B2S_TRY(once_per_device(once, ctx->device, [&]() -> b2s_status {
         for (int k = 0; k < NK; ++k) {
             B2S_CUDA(cudaFuncSetAttribute(kern[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)SMEM));
@@ -2019,7 +1462,8 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
                         (size_t)fa.sharedSizeBytes, fa.numRegs, occ[k]);
             }
         }
-    }
+        return B2S_OK;
+    }));
     const uint64_t ntiles64 = (n + TILE - 1) / TILE;
     const uint32_t ntiles = (uint32_t)ntiles64;
     LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
@@ -2059,127 +1503,43 @@ b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, 
     return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
-b2s_status launch_pipe_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
-    using SM = PipeSmem<U, VALS, THREADS, ITEMS>;
-    constexpr int TILE = SM::TILE;
-    constexpr size_t SMEM = SM::bytes;
-    auto kern = onesweep_pipe_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>;
-    static int occ = -1;
-    static std::atomic<unsigned long long> set_on{0};
-    if (first_on_device(set_on, ctx->device)) {
-        B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-        int o = 0;
-        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, SMEM));
-        occ = o > 0 ? o : 1;
-    }
-    const uint64_t ntiles64 = (n + TILE - 1) / TILE;
-    const uint32_t ntiles = (uint32_t)ntiles64;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ * ctx->num_sms);
-    LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
-    const int slots = (int)sizeof(U);
-    for (int s = 0; s < slots; ++s) {
-        ctx->ev_pass[s] = record(ctx);
-        kern<<<grid, THREADS, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
-                                                   region[(s + 1) & 1]);
-        B2S_LAUNCHED();
-    }
-    ctx->ev_pass[slots] = record(ctx);
-    return B2S_OK;
-}
+// Tile configuration of a sort: threads x items per CTA, CTAs per SM
+// (registers must stay <= 65536 / (threads * minb) for minb CTAs per SM). The
+// defaults fill the 2-CTA/SM shared-memory budget (two tile buffers of keys
+// and payloads + 8 KB of counters per CTA). Alternatives measured in round 1
+// (256x16x4, 1024x16x1, 512x20/22x2, 1024x24x1, 384x20x3, 256x24x4 for u32;
+// 512x10 and 1024x12 for u32+payload and u64; 512x6/8 for u64+payload, and
+// the software-pipelined and warp-specialised kernels) were all slower; their
+// numbers are in DESIGN.md and their code in the history (commit d25c4e5).
+struct TileCfg {
+    int threads, items, minb;
+};
 
-template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
-b2s_status launch_pipe_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
-    if (ctx->atomic_rank)
-        return launch_pipe_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb);
-    return launch_pipe_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
+TileCfg tile_cfg(int kbytes, bool vals, uint64_t n) {
+    if (kbytes == 4 && vals) return {512, 12, 2};
+    // small sorts (the partitions of cfg1) are latency-bound: smaller tiles,
+    // more CTAs (2^20 keys, p = 4: 0.088 vs 0.095 ms per partitioned sort)
+    if (kbytes == 4) return n < kTwinMinKeys ? TileCfg{512, 16, 2} : TileCfg{512, 24, 2};
+    // 8-byte keys + payload: one 1024-thread CTA per SM with 8192-pair tiles
+    // (per 2^28-pair pass 1.92 ms vs 1.97 for two 512-thread CTAs with
+    // 4096-pair tiles)
+    if (vals) return {1024, 8, 1};
+    return {512, 12, 2};
 }
-
-template <typename U, bool VALS, typename LB, int ITEMS>
-b2s_status launch_ws_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
-    using SM = WsSmem<U, VALS, ITEMS>;
-    constexpr int TILE = SM::TILE;
-    constexpr size_t SMEM = SM::bytes;
-    auto kern = onesweep_ws_kernel<U, VALS, LB, ITEMS>;
-    static int occ = -1;
-    static std::atomic<unsigned long long> set_on{0};
-    if (first_on_device(set_on, ctx->device)) {
-        B2S_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-        int o = 0;
-        B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 512, SMEM));
-        occ = o > 0 ? o : 1;
-    }
-    const uint64_t ntiles64 = (n + TILE - 1) / TILE;
-    const uint32_t ntiles = (uint32_t)ntiles64;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)occ * ctx->num_sms);
-    LB* region[2] = {static_cast<LB*>(lb), static_cast<LB*>(lb) + (size_t)ntiles * kRadix};
-    const int slots = (int)sizeof(U);
-    for (int s = 0; s < slots; ++s) {
-        ctx->ev_pass[s] = record(ctx);
-        kern<<<grid, 512, SMEM, ctx->stream>>>(plan, ctr, s, n, ntiles, region[s & 1],
-                                               region[(s + 1) & 1]);
-        B2S_LAUNCHED();
-    }
-    ctx->ev_pass[slots] = record(ctx);
-    return B2S_OK;
-}
-
-// smallest tile over all configurations: sizes the look-back scratch
-constexpr int kMinTile = 512 * 6;  // smallest tile of any configuration (u64 + payload, cfg 1)
 
 template <typename U, bool VALS, typename LB>
 b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
-    // Defaults fill the 2-CTA/SM shared-memory budget (two tile buffers of
-    // keys and payloads + 8 KB of counters per CTA); other configurations are
-    // tuning alternatives (B2S_ONESWEEP_CFG), kept with their measured results
-    // in DESIGN.md.
-    const int cfg = onesweep_cfg();
-#ifdef B2S_DEV_FAST
-    // development builds (tools/kdev_build.sh, -DB2S_DEV_FAST): only the default
-    // u32 keys-only pass is compiled, for quick kernel iteration
-    if constexpr (sizeof(U) == 4 && !VALS) {
-        // occupancy experiments (per 2^28 u32 pass): 3 x 384 thr x 20 items
-        // 0.776 ms, 4 x 256 x 24 0.891, default 2 x 512 x 24 0.722
-        if (cfg == 12) return launch_passes_cfg<U, VALS, LB, 384, 20, 3>(ctx, plan, ctr, n, lb);
-        if (cfg == 13) return launch_passes_cfg<U, VALS, LB, 256, 24, 4>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
-    }
-    return B2S_EINVAL;
-#else
+    const TileCfg c = tile_cfg((int)sizeof(U), VALS, n);
     if constexpr (sizeof(U) == 4 && VALS) {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 256, 16, 4>(ctx, plan, ctr, n, lb);
-        // small sorts (the partitions of cfg1) are latency-bound: smaller tiles,
-        // more CTAs (2^20 keys, p = 4: 0.088 vs 0.095 ms per partitioned sort)
-        if (cfg == 2 || (cfg == 0 && n < kTwinMinKeys))
-            return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 1024, 16, 1>(ctx, plan, ctr, n, lb);
-        if (cfg == 4) return launch_passes_cfg<U, VALS, LB, 512, 20, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 5) return launch_passes_cfg<U, VALS, LB, 512, 22, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 11) return launch_passes_cfg<U, VALS, LB, 1024, 24, 1>(ctx, plan, ctr, n, lb);
-        if (cfg == 9 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 24>(ctx, plan, ctr, n, lb);
-        if (cfg == 10 && ctx->atomic_rank) return launch_ws_cfg<U, VALS, LB, 20>(ctx, plan, ctr, n, lb);
-        if (cfg == 6) return launch_pipe_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 8) return launch_pipe_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
+        if (c.items == 16) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 24, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
-        // 8-byte keys + payload: one 1024-thread CTA per SM with 8192-pair
-        // tiles (per 2^28-pair pass 1.92 ms vs 1.97 for two 512-thread CTAs
-        // with 4096-pair tiles, cfg 3; the other key types measured faster
-        // with two CTAs: u32 0.72 vs 0.79, u32+payload 1.33 vs 1.37, u64 1.27
-        // vs 1.32 ms, tools/cfgab.sh)
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 6, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 3) return launch_passes_cfg<U, VALS, LB, 512, 8, 2>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 1024, 8, 1>(ctx, plan, ctr, n, lb);
     } else {
-        if (cfg == 1) return launch_passes_cfg<U, VALS, LB, 512, 10, 2>(ctx, plan, ctr, n, lb);
-        if (cfg == 2) return launch_passes_cfg<U, VALS, LB, 1024, 12, 1>(ctx, plan, ctr, n, lb);
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     }
-#endif
 }
 
 template <typename U, bool VALS>
@@ -2187,7 +1547,7 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
                         const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc) {
     constexpr int NP = sizeof(U);
     const uint32_t top_xor = is_signed ? 0x80u : 0u;
-    const size_t lb_region = lookback_region_bytes(n);
+    const size_t lb_region = lookback_region_bytes(n, (int)sizeof(U), VALS);
     SortScratch own;
     if (sc == nullptr) {
         B2S_TRY(ctx->hist.ensure(sizeof(RadixCounters)));
@@ -2210,10 +1570,12 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     // pairs' passes gain nothing from skipping the in-pass count (1.96 ms)
     const bool all_hist = n >= kAllHistMinKeys && all_hist_mode() >= (sizeof(U) == 4 ? 1 : 2);
     if (all_hist) {
-        static std::atomic<unsigned long long> set_on{0};
-        if (first_on_device(set_on, ctx->device))
+        static DeviceOnce once;
+        B2S_TRY(once_per_device(once, ctx->device, [&]() -> b2s_status {
             B2S_CUDA(cudaFuncSetAttribute(radix_prologue_all_kernel<U>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAllHistSmem));
+            return B2S_OK;
+        }));
         const uint64_t want = (n / (16 / sizeof(U)) + kAllHistThreads * 4 - 1) / (kAllHistThreads * 4);
         const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)ctx->num_sms);
         radix_prologue_all_kernel<U><<<grid, kAllHistThreads, kAllHistSmem, ctx->stream>>>(
@@ -2313,8 +1675,10 @@ extern "C" int b2s_debug_phase_cycles(unsigned long long* out16, int reset) {
 }
 #endif
 
-size_t lookback_region_bytes(uint64_t n) {
-    const uint64_t ntiles = (n + kMinTile - 1) / kMinTile;
+size_t lookback_region_bytes(uint64_t n, int kbytes, bool vals) {
+    const TileCfg c = tile_cfg(kbytes, vals, n);
+    const uint64_t tile = (uint64_t)c.threads * c.items;
+    const uint64_t ntiles = (n + tile - 1) / tile;
     return ntiles * kRadix * (n >= (1ull << 30) ? 8 : 4);
 }
 
@@ -2322,6 +1686,20 @@ b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout
                       const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc) {
     const bool sgn = key_signed(dtype);
     const bool vals = vin != nullptr;
+    // The pass plan's buffer chain treats keys and payload alike (in place or
+    // not). Mixed aliasing -- keys in place with the payload out of place or
+    // the reverse -- first copies the out-of-place array to its destination
+    // and then sorts both in place.
+    if (vals && n > 0 && (kin == kout) != (vin == vout)) {
+        if (kin == kout) {
+            B2S_CUDA(cudaMemcpyAsync(vout, vin, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            vin = vout;
+        } else {
+            B2S_CUDA(cudaMemcpyAsync(kout, kin, n * (size_t)key_bytes(dtype), cudaMemcpyDeviceToDevice,
+                                     ctx->stream));
+            kin = kout;
+        }
+    }
     if (key_bytes(dtype) == 4) {
         return vals ? radix_sort_t<uint32_t, true>(ctx, sgn, kin, kout, vin, vout, n, sc)
                     : radix_sort_t<uint32_t, false>(ctx, sgn, kin, kout, vin, vout, n, sc);

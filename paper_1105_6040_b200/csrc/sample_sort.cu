@@ -154,11 +154,13 @@ b2s_status select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int count, 
     int m = 1;
     while (m < count) m <<= 1;
     const size_t smem = (size_t)m * sizeof(b2s_sample);
-    static std::atomic<unsigned long long> set_on{0};
-    if (first_on_device(set_on, ctx->device))
+    static DeviceOnce once;
+    B2S_TRY(once_per_device(once, ctx->device, [&]() -> b2s_status {
         B2S_CUDA(cudaFuncSetAttribute(select_splitters_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(kSelectMax * sizeof(b2s_sample))));
+        return B2S_OK;
+    }));
     select_splitters_kernel<<<1, 1024, smem, ctx->stream>>>(samples, count, nparts, splitters);
     B2S_LAUNCHED();
     return B2S_OK;

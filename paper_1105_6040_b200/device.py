@@ -325,6 +325,20 @@ class Context:
                                  B2S_DEVICE))
         return out
 
+    def gen_zipf(self, n: int, seed: int, thresholds, dtype=None, first: int = 0, out=None,
+                 stream=None):
+        """cfg4a's Zipf keys on the device: key_i = #{r : thresholds[r] <= z_{first+i} >> 11}
+        (thresholds: ascending uint64 numpy array, see workloads.zipf_thresholds)."""
+        t = np.ascontiguousarray(thresholds, dtype=np.uint64)
+        if out is None:
+            out = torch.empty(n, dtype=dtype or torch.int32, device=f"cuda:{self.device}")
+        host = _is_host(out)
+        if not host:
+            self._bind_stream(stream)
+        check(lib().b2s_gen_zipf(self._h, dtype_code(out), first, n, seed, t.ctypes.data,
+                                 t.size, _ptr(out), B2S_HOST if host else B2S_DEVICE))
+        return out
+
     def check_sorted(self, keys, stream=None):
         """(adjacent inversions, order-sensitive fingerprint, multiset hash)."""
         inv, fp, ms = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()

@@ -133,8 +133,10 @@ def merge_sort(block, first: int, last: int, scratch=None) -> None:
 
 def quick_sort(block, start: int, length: int) -> None:
     """kernels::quick_sort on [start, start+length) (P/src/sort_core.cpp:135-144);
-    an out-of-range segment raises ProgrammingError as the reference does."""
-    if start + length > len(block):
+    an out-of-range segment raises ProgrammingError as the reference does.
+    The reference takes size_t, so a negative start or length (which Python
+    slicing would wrap around) is out of range too."""
+    if start < 0 or length < 0 or start + length > len(block):
         raise ProgrammingError(f"quick_sort segment out of range: start={start} "
                                f"length={length} size={len(block)}")
     _sort_inplace(block, start, start + length)

@@ -90,6 +90,11 @@ def test_kernel_edge_semantics():
     assert v.tolist() == [2, 1]
     with pytest.raises(ProgrammingError):
         sb.quick_sort(np.array([1, 2], dtype=np.int64), 1, 2)
+    # size_t arguments in the reference: negative values are out of range, not
+    # Python's wrap-around slices
+    for start, length in ((-1, 1), (0, -1), (-2, 2)):
+        with pytest.raises(ProgrammingError):
+            sb.quick_sort(np.array([3, 2, 1], dtype=np.int64), start, length)
     # sub-range sorts leave the rest alone
     v = np.array([9, 5, 3, 1, 0], dtype=np.int64)
     sb.merge_sort(v, 1, 3)

@@ -38,15 +38,3 @@ def test_sort_suite_under_rank_mode(env, sel):
                         os.path.join(HERE, "test_gpu_sort.py"), "-k", sel],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-
-
-@pytest.mark.parametrize("cfg", ["1", "2", "3", "4", "5", "6", "8", "9", "10", "11"])
-def test_tile_configuration_sorts(cfg):
-    """Every selectable tile configuration (B2S_ONESWEEP_CFG: other tile
-    shapes, the software-pipelined and the warp-specialised variants) still
-    sorts correctly."""
-    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "tools", "cfg_check.py")],
-                       env=dict(os.environ, B2S_ONESWEEP_CFG=cfg), capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "MISMATCH" not in r.stdout and r.stdout.count("OK") == 3, \
-        r.stdout[-2000:] + r.stderr[-2000:]

@@ -112,6 +112,35 @@ def test_sort_in_place_and_host_buffers(ctx, dt):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("kind", ["equal", "topbyte", "uniform", "dups"])
+@pytest.mark.parametrize("n", [5000, 300_000, 5_000_000])
+def test_sort_pairs_mixed_aliasing(ctx, dt, kind, n):
+    """Keys sorted in place with the payload in a separate buffer, and the
+    reverse: all-equal keys execute 0 passes, topbyte keys 1 (an odd count), so
+    both exercise the trailing-copy and buffer-chain corner cases."""
+    rng = np.random.default_rng(n + 3)
+    keys = rand_keys(n, dt, rng, kind)
+    vals = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    ek, ev = oracle.stable_sort_kv(keys, vals)
+    tv = lambda x: torch.from_numpy(x.view(np.int32)).cuda()  # noqa: E731
+    # keys in place, payload out of place
+    dk, dv = to_dev(keys), tv(vals)
+    dvo = torch.full_like(dv, -1)
+    ctx.sort(dk, out=dk, vals=dv, vals_out=dvo)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(dk, dt), ek)
+    assert np.array_equal(dvo.cpu().numpy().view(np.uint32), ev)
+    # keys out of place, payload in place
+    dk, dv = to_dev(keys), tv(vals)
+    dko = torch.empty_like(dk)
+    ctx.sort(dk, out=dko, vals=dv, vals_out=dv)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(dko, dt), ek)
+    assert np.array_equal(dv.cpu().numpy().view(np.uint32), ev)
+    assert np.array_equal(to_host(dk, dt), keys)  # input keys untouched
+
+
+@pytest.mark.parametrize("dt", DTYPES)
 @pytest.mark.parametrize("kind", ["dups", "uniform", "equal", "skewed", "sorted", "reverse"])
 @pytest.mark.parametrize("n", [123_457, 3072, 5121, 1, 8191, 8192, 8193, 16385])
 def test_sort_pairs_stable(ctx, dt, kind, n):

@@ -1,6 +1,6 @@
 #!/bin/bash
-# Development build of radix_sort.cu (u32 default onesweep path only, see
-# B2S_DEV_FAST) linked with the other prebuilt objects:
+# Development build of radix_sort.cu with extra -D switches, linked with the
+# other prebuilt objects:
 #   bash tools/kdev_build.sh NAME "-DFOO=1"  ->  paper_1105_6040_b200/lib/libb200sort_NAME.so
 set -e
 cd "$(dirname "$0")/.."
@@ -8,7 +8,7 @@ name=$1
 defs=$2
 mkdir -p build/dev_$name
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    -Iinclude -Ipaper_1105_6040_b200/csrc --expt-relaxed-constexpr -diag-suppress 177 -DB2S_DEV_FAST $defs \
+    -Iinclude -Ipaper_1105_6040_b200/csrc --expt-relaxed-constexpr -diag-suppress 177 $defs \
     -Xptxas -v -c paper_1105_6040_b200/csrc/radix_sort.cu -o build/dev_$name/radix_sort.o 2> build/dev_$name/ptxas.txt \
     || (cat build/dev_$name/ptxas.txt; exit 1)
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_1105_6040_b200/lib/libb200sort_$name.so \
