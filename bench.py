@@ -2,20 +2,26 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N=1 workload (BASELINE.json configs[1], "cfg2"): 2^28 uint32 keys, the
-gen_data splitmix64 stream (seed 1) >> 32, i.e. uniform over the full 32-bit
-range, p=1 -- a pure local radix sort, 4 digit passes of 8 bits. One step =
-one b2s_sort of the 1 GiB key array, input resident in HBM (inputs are larger
-than L2, so no flush is needed between steps).
+Workload at every N: BASELINE.json configs[2] ("cfg3"), 2^31 int32 keys, the
+gen_data splitmix64 stream (seed 1) >> 33, i.e. uniform over [0, 2^31), the
+metric's "int32 at 1/2/4/8 B200" series. The total is fixed (strong scaling).
 
-N>1 (torchrun, one process per GPU, NCCL): the multi-GPU sample sort of
-configs[2] with 2^28 int32 keys per GPU (2^31 total at N=8; weak scaling):
+N=1: one GPU sorts all 2^31 keys (a pure local radix sort, 4 digit passes of
+8 bits; the exchange of the sample sort is empty at G=1). One step = one
+b2s_sort of the 8 GiB key array, input resident in HBM (larger than L2, so no
+flush is needed). The line also carries cfg2's per-pass roofline (2^28 uint32,
+BASELINE.json configs[1]) measured in the same run.
+
+N>1 (torchrun, one process per GPU): the multi-GPU sample sort of the same
+2^31 keys, shard r = plan_partition(2^31, N)[r] contiguous keys of the stream:
 local sort, 64 regular samples per GPU, all-gather, splitters, bucket bounds,
-NCCL all-to-all, k-way merge of the received runs.
+exchange (merge kernels pull from peers over NVLink, or NCCL all-to-all), k-way
+merge of the received runs.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libsortbench_ref.so, parallel::scatter_merge_sort, merge, p = k =
-host threads) on a bounded sample of the same workload.
+host threads) on the largest power-of-two sample of the workload that fits
+the host's memory and the run's time budget (stated in the line).
 """
 from __future__ import annotations
 
@@ -44,15 +50,16 @@ def _peaks():
         return 6650.0, "fallback"
 
 
-def _traffic(n):
-    """DRAM bytes per onesweep launch from the committed ncu --set full capture
-    (profiles/*_onesweep_traffic.json, newest round), when it matches n."""
+def _traffic(_n, alg_bytes):
+    """DRAM bytes per onesweep launch from the committed ncu --set full
+    captures (profiles/r*_onesweep_traffic*.json, newest round first) of the
+    launch with the same algorithmic bytes."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_onesweep_traffic.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_onesweep_traffic*.json")))
     for f in reversed(files):
         try:
             d = json.load(open(f))
-            if d.get("algorithmic_bytes_per_launch") == 8 * n:
+            if d.get("algorithmic_bytes_per_launch") == alg_bytes:
                 return d["traffic_bytes_per_launch"]
         except Exception:
             continue
@@ -119,21 +126,63 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # reference CPU arm (oracle/_ref = the reference library compiled from source)
 
-WORKLOAD_1 = "cfg2: 2^28 uint32 keys, p=1, 4 x 8-bit LSD passes"
-WORKLOAD_N = "cfg3: sample sort, 2^28 int32 keys per GPU, 64 samples/GPU"
+N_TOTAL = 1 << 31
+WORKLOAD = ("cfg3: 2^31 int32 keys (gen_data >> 33), sharded over the GPUs by plan_partition; "
+            "G=1: one local radix sort (4 x 8-bit LSD passes), G>1: sample sort with 64 "
+            "samples/GPU")
+REF_BYTES_PER_KEY = 44  # peak RSS of scatter_merge_sort: 5.4 int64 copies
 
 
-def cpu_reference(sample_n: int, reps: int = 3, shift: int = 32):
-    """parallel::scatter_merge_sort (merge, wall mode, p = k = host threads) on
-    `sample_n` keys of the workload's distribution widened to int64 (the
-    reference's only Element type); run_benchmark's semantics: median of reps
-    of the world's wall seconds (P/src/bench.cpp:106-169)."""
+def _mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
+
+
+def _ref_keys(n: int, shift: int = 33):
+    """The workload's keys widened to int64 (the reference's only Element type)."""
     import numpy as np
 
     import oracle
+    z = oracle.gen_data(n, 1).view(np.uint64)
+    return (z >> np.uint64(shift)).astype(np.int64)
+
+
+def ref_sample_size(budget_s: float, cap: int = N_TOTAL) -> tuple[int, str]:
+    """Largest power of two <= cap whose reference run fits in half the host's
+    available memory (44 B/key) and, extrapolated n log n from a 2^22 probe,
+    in budget_s seconds."""
+    import oracle
     threads = max(1, min(os.cpu_count() or 1, 64))
-    z = oracle.gen_data(sample_n, 1).view(np.uint64)
-    data = (z >> np.uint64(shift)).astype(np.int64)
+    if not oracle.ref_available():
+        return 1 << 22, "oracle port (reference library not built)"
+    probe = 1 << 22
+    _, t = oracle.ref_scatter_merge_sort(_ref_keys(probe), threads, "merge", cores=threads, wall=True)
+    mem = _mem_available() // 2
+    n = probe
+    while n * 2 <= cap:
+        m = n * 2
+        est = t * (m / probe) * ((m.bit_length() - 1) / 22)
+        if est > budget_s or m * REF_BYTES_PER_KEY > mem:
+            break
+        n = m
+    why = (f"largest power of two within half the host's available memory ({mem >> 30} GiB at "
+           f"{REF_BYTES_PER_KEY} B/key) and ~{budget_s:.0f} s per run (2^22 probe: {t:.3f} s)")
+    return n, why
+
+
+def cpu_reference(sample_n: int, reps: int = 3, shift: int = 33):
+    """parallel::scatter_merge_sort (merge, wall mode, p = k = host threads) on
+    `sample_n` keys of the workload's distribution widened to int64;
+    run_benchmark's semantics: median of reps of the world's wall seconds
+    (P/src/bench.cpp:106-169)."""
+    import oracle
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    data = _ref_keys(sample_n, shift)
     if oracle.ref_available():
         kind = "reference"
         times = []
@@ -157,13 +206,15 @@ def cpu_reference(sample_n: int, reps: int = 3, shift: int = 32):
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
-    sample_n = args.ref_sample
-    multi = max(args.gpus, world) > 1
-    shift = 33 if multi else 32  # cfg3 int32 in [0, 2^31) / cfg2 full-range uint32
+    # every step is one reference run; the whole --steps/--warmup run stays
+    # within ~4 minutes
+    per_step = 240.0 / max(1, args.steps + args.warmup)
+    sample_n, why = (args.ref_sample, "set by --ref-sample") if args.ref_sample else \
+        ref_sample_size(per_step)
     vals = []
     base = None
     for i in range(args.warmup + args.steps):
-        b = cpu_reference(sample_n, reps=1, shift=shift)
+        b = cpu_reference(sample_n, reps=1)
         if i >= args.warmup:
             vals.append(b["value"])
         base = b
@@ -172,11 +223,12 @@ def run_reference_arm(args, rank: int, world: int):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic (gen_data splitmix64 seed 1)",
-        "config": {"workload": WORKLOAD_N if multi else WORKLOAD_1, "sample_n": sample_n,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (gen_data splitmix64 seed 1 >> 33)",
+        "config": {"workload": WORKLOAD, "n": N_TOTAL, "sample_n": sample_n, "sample_why": why,
                    "p": base["cores"], "algorithm": "merge",
-                   "note": "reference CPU path on a bounded sample of the workload"},
+                   "note": "reference CPU path (host cores of the GPU box) on a bounded sample "
+                           "of the workload"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
                          "sample": base["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -186,6 +238,37 @@ def run_reference_arm(args, rank: int, world: int):
 
 # ---------------------------------------------------------------------------
 # B200 arm, N = 1
+
+def _pass_roofline(ctx, keys, out, reps, hbm_peak, peak_kind, kbytes, kernel):
+    """Per-pass CUDA-event durations of the onesweep launches (events recorded
+    inside the ABI on the launching stream) -> the roofline object."""
+    ctx.enable_timing(True)
+    pass_ms, hist_ms, executed = [], [], 0
+    for _ in range(reps):
+        ctx.sort(keys, out=out)
+        t = ctx.timing()
+        pass_ms.extend(t.pass_ms)
+        hist_ms.append(t.hist_ms)
+        executed = t.passes_executed
+    ctx.enable_timing(False)
+    n = keys.numel()
+    avg_pass = statistics.mean(pass_ms)
+    alg = 2 * kbytes * n  # read + write of every key per pass
+    achieved = alg / (avg_pass * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": _traffic(n, alg),
+            "kernel": kernel, "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": alg, "avg_launch_ms": avg_pass}
+    phases = {"hist_plus_plan": statistics.mean(hist_ms), "pass_avg": avg_pass,
+              "passes_executed": executed}
+    return roof, phases
+
+
+def _plan_partition(n: int, p: int):
+    """plan_partition (P/src/parallel_sort.cpp:26-38): the first n mod p ranks
+    get one extra key."""
+    return [n // p + (1 if r < n % p else 0) for r in range(p)]
+
 
 def run_single(args):
     import numpy as np
@@ -198,16 +281,22 @@ def run_single(args):
     torch.cuda.set_device(0)
     ctx = Context(0)
     n = args.n
-    keys = ctx.gen_keys(n, 1, torch.uint32, shift=32)
+    keys = ctx.gen_keys(n, 1, torch.int32, shift=33)
     out = torch.empty_like(keys)
     torch.cuda.synchronize()
 
-    # correctness gate on the benchmarked data (untimed, like verify_output)
+    # correctness gate on the benchmarked data (untimed, like verify_output):
+    # sorted, a permutation of the input and, at the golden size, equal to the
+    # CPU-computed expected output (tests/golden/fullsize.json)
     _, _, ms_in = ctx.check_sorted(keys)
     ctx.sort(keys, out=out)
-    inv, _, ms_out = ctx.check_sorted(out)
+    inv, fp, ms_out = ctx.check_sorted(out)
     if inv != 0 or ms_in != ms_out:
         raise RuntimeError("bench: sorted output failed verification")
+    gold = _golden("cfg3")
+    golden_ok = (fp == int(gold["fp"])) if gold and gold["n"] == n else None
+    if golden_ok is False:
+        raise RuntimeError("bench: sorted output differs from the golden fingerprint")
 
     for _ in range(args.warmup):
         ctx.sort(keys, out=out)
@@ -228,28 +317,40 @@ def run_single(args):
     launches = _lib.lib().b2s_kernel_launches() - launches0
     total_ms = e0.elapsed_time(e1)
     ms_step = total_ms / args.steps
-
-    # per-kernel durations (CUDA events around each launch inside the ABI)
-    ctx.enable_timing(True)
-    pass_ms, hist_ms, executed = [], [], 0
-    for _ in range(args.steps):
-        ctx.sort(keys, out=out)
-        t = ctx.timing()
-        pass_ms.extend(t.pass_ms)
-        hist_ms.append(t.hist_ms)
-        executed = t.passes_executed
-    ctx.enable_timing(False)
+    roof, phases = _pass_roofline(ctx, keys, out, args.steps, hbm_peak, peak_kind, 4,
+                                  "onesweep_kernel (one digit pass of 2^31 int32 keys)")
     clk = clocks.stop()
 
-    # end to end through the C ABI with pinned HOST buffers (H2D + sort + D2H)
+    # cfg2's per-pass roofline (2^28 uint32, BASELINE.json configs[1]), same run
+    k2 = ctx.gen_keys(1 << 28, 1, torch.uint32, shift=32)
+    o2 = torch.empty_like(k2)
+    for _ in range(3):
+        ctx.sort(k2, out=o2)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        ctx.sort(k2, out=o2)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    roof2, phases2 = _pass_roofline(ctx, k2, o2, args.steps, hbm_peak, peak_kind, 4,
+                                    "onesweep_kernel (one digit pass of 2^28 uint32 keys)")
+    roof2["sort_ms"] = t0.elapsed_time(t1) / args.steps
+    roof2["keys_per_s"] = (1 << 28) / (roof2["sort_ms"] * 1e-3)
+    roof2["phases_ms"] = phases2
+    del k2, o2
+
+    # end to end through the C ABI with pinned HOST buffers (H2D + sort + D2H),
+    # a stream of host batches through b2s_sort_batch: batch i+1 uploads while
+    # batch i sorts and batch i-1 downloads (PCIe full duplex)
     h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    h_in.copy_(keys.view(torch.int32).cpu())
+    h_in.copy_(keys.cpu())
     h_out = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    hin_np = h_in.numpy().view(np.uint32)
-    hout_np = h_out.numpy().view(np.uint32)
-    # a stream of K host batches through b2s_sort_batch: batch i+1 uploads
-    # while batch i sorts and batch i-1 downloads (PCIe full duplex)
-    e2e_steps = max(2, args.steps)
+    del out
+    torch.cuda.empty_cache()
+    hin_np = h_in.numpy()
+    hout_np = h_out.numpy()
+    e2e_steps = max(3, min(args.steps, 6))
     ctx.sort_batch([hin_np] * 3, outs=[hout_np] * 3)  # warm the three staging buffers
     t0 = time.perf_counter()
     ctx.sort_batch([hin_np] * e2e_steps, outs=[hout_np] * e2e_steps)
@@ -260,30 +361,26 @@ def run_single(args):
     ctx.sort(hin_np, out=hout_np)  # one unpipelined call, for reference
     e2e_single_s = time.perf_counter() - t0
 
-    avg_pass = statistics.mean(pass_ms)
-    alg_bytes = 2 * 4 * n  # read + write of every 4-byte key per pass
-    achieved = alg_bytes / (avg_pass * 1e-3) / 1e9
     value = n / (ms_step * 1e-3)
-    cpu = cpu_reference(args.cpu_sample, reps=3, shift=32) if not args.no_cpu else None
+    cpu = None
+    if not args.no_cpu:
+        cpu_n, why = ref_sample_size(6.0)
+        cpu = cpu_reference(cpu_n, reps=3)
+        cpu["sample_why"] = why
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (gen_data splitmix64 seed 1 >> 32, uniform 32-bit)",
-        "config": {"workload": WORKLOAD_1,
-                   "n": n, "p": 1, "key_bytes": 4,
-                   "l2": "inputs (1 GiB) larger than L2; no flush"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": _traffic(n),
-                     "kernel": "onesweep_kernel (one digit pass)",
-                     "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "avg_launch_ms": avg_pass},
-        "phases_ms": {"hist_plus_plan": statistics.mean(hist_ms),
-                      "pass_avg": avg_pass, "passes_executed": executed},
+        "scaling": "strong", "vs_baseline": None, "dtype": "i32",
+        "data": "synthetic (gen_data splitmix64 seed 1 >> 33, int32 uniform in [0, 2^31))",
+        "config": {"workload": WORKLOAD, "n": n, "p": 1, "key_bytes": 4,
+                   "golden_fingerprint_match": golden_ok,
+                   "l2": "inputs (8 GiB) larger than L2; no flush"},
+        "roofline": roof,
+        "phases_ms": phases,
+        "roofline_cfg2": roof2,
         "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
                 "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_s * 1e3,
-                "path": f"b2s_sort_batch(B2S_HOST) over {e2e_steps} pinned host batches "
+                "path": f"b2s_sort_batch(B2S_HOST) over {e2e_steps} pinned 8 GiB host batches "
                         "(upload/sort/download of consecutive batches overlapped)",
                 "single_call_ms": e2e_single_s * 1e3},
         "gpu_launches": launches,
@@ -292,6 +389,17 @@ def run_single(args):
     }
     print(json.dumps(line), flush=True)
     ctx.close()
+
+
+def _golden(name):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "fullsize.json")) as f:
+            for c in json.load(f)["configs"]:
+                if c["config"] == name:
+                    return c
+    except Exception:
+        pass
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -309,13 +417,20 @@ def run_multi(args, rank: int, world: int):
     hbm_peak, peak_kind = _peaks()
     nvlink_gbs = 770.0  # measured peer copy per direction (B200_PROFILING.md)
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if rank == 0:  # NCCL's communicator-init lines (rank count) on rank 0's stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    print(f"[bench] rank {rank}/{world} on cuda:{local}: NCCL process group up", file=sys.stderr,
+          flush=True)
     ctx = Context(local)
-    n_local = args.n_per_gpu
-    total = n_local * world
-    # shard r holds keys [r*n_local, (r+1)*n_local) of the cfg3 stream (int32 = z >> 33)
-    keys = ctx.gen_keys(n_local, 1, torch.int32, shift=33, first=rank * n_local)
+    total = args.n
+    sizes = _plan_partition(total, world)
+    n_local = sizes[rank]
+    first = sum(sizes[:rank])
+    # shard r = plan_partition's r-th contiguous slice of the cfg3 stream (int32 = z >> 33)
+    keys = ctx.gen_keys(n_local, 1, torch.int32, shift=33, first=first)
     transport, transport_note = args.transport, None
     if transport == "p2p":
         probe = SampleSorter(ctx, transport="p2p")
@@ -401,20 +516,20 @@ def run_multi(args, rank: int, world: int):
     avg_pass = statistics.mean(pass_ms)
     alg = 2 * 4 * n_local
     achieved = alg / (avg_pass * 1e-3) / 1e9
-    # combined roofline per GPU (serial, non-overlapped): 4 sort passes +
-    # merge rounds over HBM, (G-1)/G of the shard over NVLink each direction
-    rounds = max(1, (world - 1).bit_length()) if world > 1 else 0
-    hbm_bytes = (4 * 2 * 4 + 4 + rounds * 2 * 4) * n_local
+    # combined roofline per GPU (serial, non-overlapped): the
+    # prologue read, 4 sort passes and ONE merge pass over HBM, (G-1)/G of the
+    # shard over NVLink each direction
+    hbm_bytes = (4 * 2 * 4 + 4 + (2 * 4 if world > 1 else 0)) * n_local
     nvl_bytes = 4 * n_local * (world - 1) / world
     t_roof_ms = (hbm_bytes / (hbm_peak * 1e9) + nvl_bytes / (nvlink_gbs * 1e9)) * 1e3
     if rank == 0:
         line = {
             "metric": METRIC, "value": total / (ms_step * 1e-3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "i32",
             "data": "synthetic (gen_data splitmix64 seed 1 >> 33, int32 in [0, 2^31))",
-            "config": {"workload": WORKLOAD_N,
+            "config": {"workload": WORKLOAD, "n": total,
                        "n_per_gpu": n_local, "parallelism": f"sample sort over {world} GPUs",
                        "exchange": ("merge kernels pull buckets from peer shards over NVLink "
                                     "(CUDA IPC)" if transport == "p2p" else
@@ -422,7 +537,7 @@ def run_multi(args, rank: int, world: int):
                        "exchange_note": transport_note,
                        "l2": "inputs larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": _traffic(n_local),
+                         "frac": achieved / hbm_peak, "traffic": _traffic(n_local, alg),
                          "kernel": "onesweep_kernel (one digit pass, rank 0)",
                          "peak_kind": peak_kind,
                          "combined_hbm_nvlink_frac": t_roof_ms / ms_step,
@@ -447,10 +562,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 28)
-    ap.add_argument("--n-per-gpu", type=int, default=1 << 28)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
-    ap.add_argument("--ref-sample", type=int, default=1 << 24)
+    ap.add_argument("--n", type=int, default=N_TOTAL, help="total keys (all GPUs)")
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="reference arm sample size (default: sized to memory and time)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU exchange: merge kernels pull from peers over NVLink "
