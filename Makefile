@@ -6,7 +6,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
 SRC := paper_1105_6040_b200/csrc
 LIB := paper_1105_6040_b200/lib
 OBJ := build/obj
-CU := abi radix_sort merge_path sample_sort gen_verify
+CU := abi radix_sort merge_path sample_sort gen_verify multi
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(CU)))
 HDRS := include/b200sort.h $(SRC)/b2s_internal.cuh
 
@@ -18,7 +18,7 @@ $(OBJ)/%.o: $(SRC)/%.cu $(HDRS)
 
 $(LIB)/libb200sort.so: $(OBJS)
 	@mkdir -p $(LIB)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -ldl
 
 # the reference's C++ signatures on top of the C ABI
 $(LIB)/libsortbench_b200.so: $(SRC)/compat/sortbench_compat.cpp include/sortbench_b200/sortbench.hpp $(LIB)/libb200sort.so

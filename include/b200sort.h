@@ -38,7 +38,8 @@ typedef enum b2s_status {
     B2S_EINVAL = 1,    /* bad argument / configuration   -> ConfigError      */
     B2S_ENOMEM = 2,    /* device or pinned allocation failed                 */
     B2S_ECUDA = 3,     /* CUDA runtime / launch error                        */
-    B2S_EINTERNAL = 4  /* internal invariant violated    -> ProgrammingError */
+    B2S_EINTERNAL = 4, /* internal invariant violated    -> ProgrammingError */
+    B2S_ENCCL = 5      /* NCCL error (init, collective, asynchronous abort) */
 } b2s_status;
 
 /* Key types. The reference sorts int64 only (Element,
@@ -185,6 +186,58 @@ b2s_status b2s_select_splitters(b2s_ctx* ctx, const b2s_sample* samples, int cou
 b2s_status b2s_bucket_bounds(b2s_ctx* ctx, b2s_dtype dtype, const void* sorted_keys,
                              uint64_t n, int rank, const b2s_sample* splitters, int nparts,
                              uint64_t* bounds);
+
+/* ---- multi-GPU sample sort in one process --------------------------------
+ * parallel::scatter_merge_sort across GPUs (P/src/parallel_sort.cpp:166-254):
+ * the reference runs p rank threads in one process (runtime::spawn_world,
+ * P/src/runtime.cpp:666-694) that scatter, sort, exchange blocks in p
+ * odd-even phases of send/recv (:217-244) and gather at the root (:246-248).
+ * Here one host thread per rank drives GPU devices[r]: local radix sort,
+ * samples_per_gpu regular samples, all-gather, splitters, bucket bounds, ONE
+ * exchange, and a k-way merge of the received runs.
+ *
+ * b2s_create_multi: one rank per entry of `devices`. A device may repeat
+ *   (emulated ranks: each rank gets its own context and stream on it). Peer
+ *   access is enabled between every pair of distinct devices; an NCCL
+ *   communicator (ncclCommInitAll, NCCL loaded at run time) is built when the
+ *   devices are distinct. Neither is an error when unavailable: the exchange
+ *   transport is chosen per call.
+ * Transport: B2S_XCHG_P2P -- the merge kernels of rank r read their bucket's
+ *   slice of every peer's sorted shard over NVLink (no receive buffer);
+ *   B2S_XCHG_NCCL -- grouped ncclSend/ncclRecv all-to-all, then the merge;
+ *   B2S_XCHG_AUTO (default) -- p2p when every pair has peer access, else NCCL.
+ * b2s_sample_sort (synchronous): shards[r] (counts[r] keys, device pointers on
+ *   devices[r], or host pointers with B2S_HOST) -> bucket r in out[r]
+ *   (capacity out_capacity[r] keys) with out_counts[r] keys. The buckets
+ *   concatenated in rank order are the ascending array, stable by global
+ *   index (shard order; ties to the lower rank), so payloads follow the
+ *   reference's stable tie rule. A bucket above its capacity fails with
+ *   B2S_EINVAL and out_counts holding the sizes needed. With 64 samples per
+ *   GPU a bucket holds at most about 2 * total / ranks keys (regular
+ *   sampling), also for all-equal keys (compound sample keys).
+ *   samples_per_gpu * ranks <= 8192. */
+#define B2S_XCHG_AUTO 0
+#define B2S_XCHG_P2P 1
+#define B2S_XCHG_NCCL 2
+typedef struct b2s_multi b2s_multi;
+typedef struct b2s_multi_timing {
+    float local_sort_ms;      /* rank 0: local radix sort + regular samples          */
+    float splitters_ms;       /* rank 0: sample all-gather, splitters, bucket bounds */
+    float exchange_merge_ms;  /* rank 0: bounds, exchange and k-way merge            */
+    float total_ms;           /* host wall time of the whole call                    */
+    int transport;            /* B2S_XCHG_P2P or B2S_XCHG_NCCL                        */
+    uint64_t max_bucket, min_bucket;
+} b2s_multi_timing;
+b2s_status b2s_create_multi(int ngpu, const int* devices, b2s_multi** out);
+b2s_status b2s_destroy_multi(b2s_multi* m);
+b2s_status b2s_multi_info(b2s_multi* m, int* ranks, int* p2p_ok, int* nccl_ok, int* nccl_version);
+b2s_status b2s_multi_set_transport(b2s_multi* m, int transport);
+b2s_status b2s_multi_get_timing(b2s_multi* m, b2s_multi_timing* out);
+b2s_status b2s_sample_sort(b2s_multi* m, b2s_dtype dtype, const void* const* shards,
+                           const uint32_t* const* shard_vals, const uint64_t* counts,
+                           void* const* out, uint32_t* const* out_vals,
+                           const uint64_t* out_capacity, uint64_t* out_counts,
+                           int samples_per_gpu, uint32_t flags);
 
 /* ---- input generation and verification ----------------------------------
  * b2s_gen_keys: key_i = (T)(z_{first+i} >> shift) where z is bench::gen_data's
