@@ -12,7 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("B2S_LIB") or os.path.join(HERE, "lib", "libb200sort.so")
 
-B2S_OK, B2S_EINVAL, B2S_ENOMEM, B2S_ECUDA, B2S_EINTERNAL = range(5)
+B2S_OK, B2S_EINVAL, B2S_ENOMEM, B2S_ECUDA, B2S_EINTERNAL, B2S_ENCCL = range(6)
+B2S_XCHG_AUTO, B2S_XCHG_P2P, B2S_XCHG_NCCL = range(3)
 B2S_I32, B2S_U32, B2S_I64, B2S_U64 = range(4)
 B2S_DEVICE, B2S_HOST = 0, 1
 
@@ -24,6 +25,8 @@ EXPORTS = [
     "b2s_merge_split_padded",
     "b2s_sample_regular", "b2s_select_splitters", "b2s_bucket_bounds", "b2s_gen_keys",
     "b2s_check_sorted", "b2s_gen_zipf", "b2s_exchange_buffer", "b2s_open_peer", "b2s_close_peers",
+    "b2s_create_multi", "b2s_destroy_multi", "b2s_multi_info", "b2s_multi_set_transport",
+    "b2s_multi_get_timing", "b2s_sample_sort",
 ]
 
 
@@ -37,6 +40,18 @@ class b2s_timing(ctypes.Structure):
         ("merge_ms", ctypes.c_float),
         ("merge_rounds", ctypes.c_int),
         ("total_ms", ctypes.c_float),
+    ]
+
+
+class b2s_multi_timing(ctypes.Structure):
+    _fields_ = [
+        ("local_sort_ms", ctypes.c_float),
+        ("splitters_ms", ctypes.c_float),
+        ("exchange_merge_ms", ctypes.c_float),
+        ("total_ms", ctypes.c_float),
+        ("transport", ctypes.c_int),
+        ("max_bucket", ctypes.c_uint64),
+        ("min_bucket", ctypes.c_uint64),
     ]
 
 
@@ -78,6 +93,12 @@ _SIGS = {
     "b2s_exchange_buffer": (_st, [_p, _u64, ctypes.POINTER(_p), _p]),
     "b2s_open_peer": (_st, [_p, _p, ctypes.POINTER(_p)]),
     "b2s_close_peers": (_st, [_p]),
+    "b2s_create_multi": (_st, [_i, _p, ctypes.POINTER(_p)]),
+    "b2s_destroy_multi": (_st, [_p]),
+    "b2s_multi_info": (_st, [_p, _p, _p, _p, _p]),
+    "b2s_multi_set_transport": (_st, [_p, _i]),
+    "b2s_multi_get_timing": (_st, [_p, ctypes.POINTER(b2s_multi_timing)]),
+    "b2s_sample_sort": (_st, [_p, _i, _p, _p, _p, _p, _p, _p, _p, _i, _u32]),
 }
 
 

@@ -396,3 +396,112 @@ def default_context(device: int = 0) -> Context:
         ctx = Context(device)
         _default[device] = ctx
     return ctx
+
+
+@dataclass
+class MultiTiming:
+    local_sort_ms: float
+    splitters_ms: float
+    exchange_merge_ms: float
+    total_ms: float
+    transport: str
+    max_bucket: int
+    min_bucket: int
+
+
+class MultiContext:
+    """One b2s_multi: the sample sort over several GPUs in this process, one
+    host thread per rank inside the library (b2s_sample_sort). `devices` may
+    repeat a device (emulated ranks)."""
+
+    TRANSPORTS = {"auto": _lib.B2S_XCHG_AUTO, "p2p": _lib.B2S_XCHG_P2P, "nccl": _lib.B2S_XCHG_NCCL}
+
+    def __init__(self, devices):
+        self.devices = [int(d) for d in devices]
+        arr = (ctypes.c_int * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        check(lib().b2s_create_multi(len(self.devices), arr, ctypes.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().b2s_destroy_multi(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def info(self) -> dict:
+        r, p, n, v = (ctypes.c_int() for _ in range(4))
+        check(lib().b2s_multi_info(self._h, ctypes.byref(r), ctypes.byref(p), ctypes.byref(n),
+                                   ctypes.byref(v)))
+        return {"ranks": r.value, "p2p": bool(p.value), "nccl": bool(n.value),
+                "nccl_version": v.value}
+
+    def set_transport(self, name: str) -> None:
+        check(lib().b2s_multi_set_transport(self._h, self.TRANSPORTS[name]))
+
+    def timing(self) -> MultiTiming:
+        t = _lib.b2s_multi_timing()
+        check(lib().b2s_multi_get_timing(self._h, ctypes.byref(t)))
+        names = {_lib.B2S_XCHG_P2P: "p2p", _lib.B2S_XCHG_NCCL: "nccl"}
+        return MultiTiming(t.local_sort_ms, t.splitters_ms, t.exchange_merge_ms, t.total_ms,
+                           names.get(t.transport, "?"), t.max_bucket, t.min_bucket)
+
+    def sample_sort(self, shards, vals=None, outs=None, out_vals=None, capacity=None,
+                    samples_per_gpu: int = 64):
+        """Sorts the shards (one per rank: CUDA tensors on that rank's device,
+        or numpy arrays) into buckets. Returns (buckets, bucket_vals): bucket
+        r holds the r-th slice of the global ascending order; with a payload
+        the order is stable by global index (shard order)."""
+        G = len(self.devices)
+        if len(shards) != G:
+            raise ValueError(f"need {G} shards")
+        host = _is_host(shards[0])
+        code = dtype_code(shards[0])
+        for x in shards:
+            _check_1d(x, "shard")
+            if _is_host(x) != host or dtype_code(x) != code:
+                raise ValueError("shards must share dtype and memory kind")
+        outs_given = outs
+        counts = [_numel(x) for x in shards]
+        total = sum(counts)
+        if capacity is None:
+            # regular sampling bounds a bucket by ~2 N / G; the slack covers
+            # the sample granularity
+            capacity = [min(total, 2 * (total // G) + 2 * samples_per_gpu * G + 1024)] * G
+        if outs is None:
+            outs = [np.empty(capacity[r], dtype=shards[0].dtype) if host else
+                    torch.empty(capacity[r], dtype=shards[r].dtype, device=f"cuda:{self.devices[r]}")
+                    for r in range(G)]
+        if vals is not None and out_vals is None:
+            out_vals = [np.empty(capacity[r], dtype=np.uint32) if host else
+                        torch.empty(capacity[r], dtype=vals[r].dtype,
+                                    device=f"cuda:{self.devices[r]}") for r in range(G)]
+        P = ctypes.c_void_p * G
+        U = ctypes.c_uint64 * G
+        oc = U()
+        st = lib().b2s_sample_sort(
+            self._h, code, P(*[_ptr(x) for x in shards]),
+            P(*[_ptr(v) for v in vals]) if vals is not None else None, U(*counts),
+            P(*[_ptr(o) for o in outs]), P(*[_ptr(o) for o in out_vals]) if out_vals is not None else None,
+            U(*capacity), oc, int(samples_per_gpu), B2S_HOST if host else B2S_DEVICE)
+        if st == _lib.B2S_EINVAL and b"exceeds out_capacity" in lib().b2s_last_error() and \
+                capacity != [total] * G and outs_given is None:
+            # a bucket outgrew the default capacity (far from regular
+            # sampling's bound): retry with room for everything
+            return self.sample_sort(shards, vals, None, None, [total] * G, samples_per_gpu)
+        check(st)
+        sizes = [int(oc[r]) for r in range(G)]
+        buckets = [outs[r][: sizes[r]] for r in range(G)]
+        bvals = [out_vals[r][: sizes[r]] for r in range(G)] if out_vals is not None else None
+        return buckets, bvals

@@ -16,7 +16,8 @@ class VerificationError(RuntimeError):
 
 
 class DeviceError(RuntimeError):
-    """CUDA / NCCL / out-of-memory failures (std::runtime_error in the shims)."""
+    """CUDA / NCCL / out-of-memory failures (std::runtime_error in the shims);
+    ``status`` is 2 (out of memory), 3 (CUDA) or 5 (NCCL)."""
 
     def __init__(self, msg: str, status: int = 3):
         super().__init__(msg)
