@@ -674,8 +674,14 @@ b2s_status partitioned_sort_dev(b2s_ctx* ctx, b2s_dtype dtype, const void* din, 
     // The p local sorts run concurrently, each on a side stream with its own
     // scratch (alt slice, look-back, counters, plan): a partition sort of a
     // few million keys fills a fraction of the SMs and is bound by its chain
-    // of dependent launches. With timing on they run in order on the stream.
-    const bool conc = !ctx->timing && p > 1;
+    // of dependent launches. Larger partitions fill the GPU on their own, and
+    // concurrent persistent passes (and the one-CTA-per-SM prologue) of
+    // several sorts then only crowd each other out (2^24 int64 keys, p = 2:
+    // 2.98 ms concurrent vs 0.9 ms for the unpartitioned sort), so they run
+    // one after the other, each on the whole GPU. With timing on they run in
+    // order on the stream.
+    constexpr uint64_t kConcMaxKeys = 1ull << 21;
+    const bool conc = !ctx->timing && p > 1 && sizes[0] <= kConcMaxKeys;
     const int nside = std::min(p, kSideStreams);
     std::vector<size_t> lb_off(p + 1, 0);
     for (int r = 0; r < p; ++r) lb_off[r + 1] = lb_off[r] + (2 * lookback_region_bytes(sizes[r], (int)ksz, dvin != nullptr) + 16 + 255) / 256 * 256;

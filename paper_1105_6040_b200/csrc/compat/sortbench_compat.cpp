@@ -6,10 +6,20 @@
 // (P/include/sortbench/runtime.hpp:93-95): host spans are staged to the device
 // inside each call (B2S_HOST). Status codes map back to the reference's
 // exceptions: EINVAL -> ConfigError, EINTERNAL -> ProgrammingError, CUDA/OOM ->
-// std::runtime_error (CLI exit 1, P/tools/sortbench.cpp:385-387).
+// std::runtime_error (CLI exit 1, P/tools/sortbench.cpp:385-387), NCCL too.
+//
+// scatter_merge_sort with 2 <= p <= G (G = the GPUs in SORTBENCH_B200_DEVICES,
+// e.g. "0,1,2,3" or "0,0,0,0" for ranks emulated on one device; default: every
+// visible GPU) runs as the multi-GPU sample sort (b2s_sample_sort), rank r on
+// the r-th listed device; otherwise as the single-device partitioned sort.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <sstream>
 #include <string>
+#include <vector>
 
 #include "b200sort.h"
 #include "sortbench_b200/sortbench.hpp"
@@ -189,6 +199,80 @@ KernelFn select_kernel(Algorithm algorithm) {
     throw ConfigError("unknown algorithm id");
 }
 
+namespace {
+// the rank -> device list of the multi-GPU path
+std::vector<int> rank_devices() {
+    std::vector<int> devs;
+    if (const char* e = std::getenv("SORTBENCH_B200_DEVICES")) {
+        std::stringstream ss(e);
+        std::string tok;
+        while (std::getline(ss, tok, ','))
+            if (!tok.empty()) devs.push_back(std::atoi(tok.c_str()));
+    } else {
+        for (int d = 0; d < b2s_device_count(); ++d) devs.push_back(d);
+    }
+    return devs;
+}
+
+// one multi context per rank count, kept for the process (like the
+// per-thread contexts); b2s_sample_sort serialises calls on one context
+b2s_multi* multi_for(int p) {
+    static std::mutex m;
+    static std::map<int, b2s_multi*> cache;
+    std::lock_guard<std::mutex> lk(m);
+    auto it = cache.find(p);
+    if (it != cache.end()) return it->second;
+    const std::vector<int> devs = rank_devices();
+    b2s_multi* mc = nullptr;
+    check(b2s_create_multi(p, devs.data(), &mc), "b2s_create_multi");
+    cache[p] = mc;
+    return mc;
+}
+
+// the p blocks of plan_partition (P/src/parallel_sort.cpp:26-38) sorted across
+// p GPUs; the buckets concatenated in rank order are the gathered result
+// (P/src/parallel_sort.cpp:246-248)
+double sample_sort_host(const DataList& data, int p, DataList& sorted) {
+    b2s_multi* mc = multi_for(p);
+    std::vector<std::uint64_t> sizes(static_cast<std::size_t>(p));
+    check(b2s_plan_partition(data.size(), p, sizes.data()), "b2s_plan_partition");
+    std::vector<const void*> shards(static_cast<std::size_t>(p));
+    std::size_t off = 0;
+    for (int r = 0; r < p; ++r) {
+        shards[static_cast<std::size_t>(r)] = data.data() + off;
+        off += sizes[static_cast<std::size_t>(r)];
+    }
+    // regular sampling bounds a bucket by ~2n/p; a larger one is retried with
+    // room for everything
+    std::uint64_t cap = std::min<std::uint64_t>(data.size(), 2 * (data.size() / p) + 64 * p * 2 + 1024);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        std::vector<DataList> buckets(static_cast<std::size_t>(p), DataList(cap));
+        std::vector<void*> outs(static_cast<std::size_t>(p));
+        for (int r = 0; r < p; ++r) outs[static_cast<std::size_t>(r)] = buckets[static_cast<std::size_t>(r)].data();
+        std::vector<std::uint64_t> caps(static_cast<std::size_t>(p), cap), counts(static_cast<std::size_t>(p), 0);
+        const b2s_status st = b2s_sample_sort(mc, B2S_I64, shards.data(), nullptr, sizes.data(), outs.data(),
+                                              nullptr, caps.data(), counts.data(), 64, B2S_HOST);
+        if (st == B2S_EINVAL && attempt == 0 && cap < data.size()) {
+            cap = data.size();
+            continue;
+        }
+        check(st, "b2s_sample_sort");
+        off = 0;
+        for (int r = 0; r < p; ++r) {
+            const auto& b = buckets[static_cast<std::size_t>(r)];
+            std::copy(b.begin(), b.begin() + static_cast<std::ptrdiff_t>(counts[static_cast<std::size_t>(r)]),
+                      sorted.begin() + static_cast<std::ptrdiff_t>(off));
+            off += counts[static_cast<std::size_t>(r)];
+        }
+        if (off != data.size()) throw ProgrammingError("sample sort lost keys");
+        b2s_multi_timing t{};
+        b2s_multi_get_timing(mc, &t);
+        return t.local_sort_ms + t.splitters_ms + t.exchange_merge_ms;
+    }
+    throw ProgrammingError("unreachable");
+}
+}  // namespace
+
 SortOutcome scatter_merge_sort(Algorithm algorithm, const DataList& data,
                                const runtime::WorldOptions& options) {
     const int p = options.procs;
@@ -207,6 +291,14 @@ SortOutcome scatter_merge_sort(Algorithm algorithm, const DataList& data,
         const char* e = std::getenv("SORTBENCH_B200_PHASES");
         return e != nullptr && std::atoi(e) != 0;
     }();
+    static const int gpus = static_cast<int>(rank_devices().size());
+    if (!phases && p >= 2 && p <= gpus) {
+        const double dev_ms = sample_sort_host(data, p, outcome.sorted);
+        outcome.world.wall_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        outcome.world.device_ms = dev_ms;
+        return outcome;
+    }
     if (phases)
         check(b2s_odd_even_sort(ctx(), B2S_I64, data.data(), outcome.sorted.data(), data.size(), p,
                                 B2S_HOST),

@@ -302,6 +302,64 @@ def experiment1(algorithms, n_per_algorithm, proc_list, core_list, seed: int = 1
     return rows, reports
 
 
+def run_benchmark_multi(config: RunConfig, devices: list, multi=None) -> RunReport:
+    """bench::run_benchmark (P/src/bench.cpp:106-169) with procs = GPUs: the
+    multi-GPU sample sort of the C ABI (b2s_sample_sort, one host thread per
+    rank) on ``devices[:procs]`` (a repeated device emulates ranks on it).
+    gen_data's int64 stream is generated shard by shard on each rank's device;
+    every repetition is verified (concatenated buckets sorted, multiset equal
+    to the input's); wall_seconds is the call's host wall time (the reference
+    times its world from spawn to join, P/src/runtime.cpp:87,689). The trace
+    has one compute (local sort), bcast (splitters) and gather (exchange +
+    merge of the rank's bucket) event per rank, from rank 0's CUDA events."""
+    import torch
+
+    from .device import Context, MultiContext
+    from .sortbench import plan_partition
+    if config.procs < 1 or config.cores < 1 or config.repetitions < 1:
+        raise ConfigError(f"invalid run configuration: {config}")
+    if config.algorithm not in ALGORITHMS:
+        raise ConfigError(f"unknown algorithm '{config.algorithm}'")
+    p = config.procs
+    if len(devices) < p:
+        raise ConfigError(f"{p} ranks need {p} devices (got {devices})")
+    devs = list(devices[:p])
+    own = multi is None
+    multi = multi or MultiContext(devs)
+    sizes = plan_partition(config.n, p).sizes
+    ctxs = {d: Context(d) for d in set(devs)}
+    try:
+        shards, off = [], 0
+        for r in range(p):
+            shards.append(ctxs[devs[r]].gen_keys(sizes[r], config.seed, torch.int64, first=off))
+            off += sizes[r]
+        ms_in = sum(ctxs[devs[r]].check_sorted(shards[r])[2] for r in range(p)) & ((1 << 64) - 1)
+        worlds = []
+        for _ in range(config.repetitions):
+            buckets, _ = multi.sample_sort(shards)
+            t = multi.timing()
+            cat = torch.cat([b.to(f"cuda:{devs[0]}") for b in buckets])
+            inv, _, ms_out = ctxs[devs[0]].check_sorted(cat) if cat.numel() else (0, 0, 0)
+            if inv != 0 or (cat.numel() and ms_out != ms_in) or cat.numel() != config.n:
+                raise VerificationError(f"run produced output that is not the sorted input: {config}")
+            a = int(round(t.local_sort_ms * 1e6))
+            b = a + int(round(t.splitters_ms * 1e6))
+            c = b + int(round(t.exchange_merge_ms * 1e6))
+            trace = []
+            for r in range(p):
+                trace += [TraceEvent(r, "compute", 0, a), TraceEvent(r, "bcast", a, b),
+                          TraceEvent(r, "gather", b, c, 8 * buckets[r].numel())]
+            counters = [{"element_moves": 0} for _ in range(p)]
+            worlds.append(WorldReport(p, config.cores, "wall", t.total_ms * 1e-3, trace, counters))
+        order = sorted(range(len(worlds)), key=lambda i: worlds[i].wall_seconds)
+        return report_from_world(config, worlds[order[(len(order) - 1) // 2]])
+    finally:
+        for c in ctxs.values():
+            c.close()
+        if own:
+            multi.close()
+
+
 def trace_from_sample_sort(config: RunConfig, per_rank_phases: list, n_per_rank: list,
                            key_bytes: int = 4) -> RunReport:
     """A multi-GPU SampleSorter run as the reference's trace: per GPU rank,

@@ -53,3 +53,15 @@ def test_cpp_parity_program_with_odd_even_phases():
                        env=dict(os.environ, SORTBENCH_B200_PHASES="1"))
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["0", "0,0", "0,0,0,0,0,0,0,0"])
+def test_cpp_parity_program_multi_gpu_path(devices):
+    """The same reference tests with scatter_merge_sort for 2 <= p <= G routed
+    through the multi-GPU sample sort (b2s_sample_sort), ranks emulated on
+    device 0 when the list repeats it."""
+    r = subprocess.run([PROG], capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, SORTBENCH_B200_DEVICES=devices))
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout

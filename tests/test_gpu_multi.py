@@ -251,3 +251,15 @@ def test_cfg5_g8_full(multis):
     g = GOLD["cfg5"]
     assert n == N and inv == 0 and ms == int(g["multiset"]) and fp == int(g["fp"])
     assert vfp == int(g["payload_fp"])
+
+
+def test_run_benchmark_multi_exp1_row():
+    """bench::run_benchmark / exp1 row (P/src/bench.cpp:106-169,211-222) with
+    procs = GPU ranks of the sample sort, verified every repetition."""
+    from paper_1105_6040_b200 import report as R
+    for m in (1, 2, 4):
+        rep = R.run_benchmark_multi(R.RunConfig("merge", 1 << 18, m, 2, 1, "wall", 2), [0] * m)
+        row = R.exp1_csv_row(rep).split(",")
+        assert row[0] == "merge" and row[2] == str(m) and float(row[4]) > 0
+        kinds = {e.kind for e in rep.world.trace}
+        assert kinds == {"compute", "bcast", "gather"} and len(rep.world.trace) == 3 * m
