@@ -59,12 +59,7 @@ namespace {
 
 constexpr int kRadix = 256;
 
-#ifndef B2S_PIPE_VEC
-#define B2S_PIPE_VEC 0
-#endif
-
-// items per thread of the 4-byte-key tile (512 threads) from 2^21 keys on:
-// the pipelined kernel's two counter sets and staging gap at two CTAs per SM
+// items per thread of the 4-byte-key tile (512 threads) from 2^21 keys on
 #ifndef B2S_U32_ITEMS
 #define B2S_U32_ITEMS 24
 #endif
@@ -513,20 +508,6 @@ struct OnesweepSmem {
     static_assert(kKeys >= (size_t)WARPS * kRadix * 4, "idle tile buffer holds the early counts");
 };
 
-// ---- bulk shared -> global stores (cp.async.bulk, bulk async-groups) ------
-__device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// the group's shared-memory reads are done (its staging may be overwritten)
-__device__ __forceinline__ void bulk_wait_read0() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-// the group's global writes are complete
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier ----------
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -678,7 +659,7 @@ struct TileShared {
 // predecessors were fetched into `lbw` by cp.async before the ranking; later
 // steps read B2S_LB_STEP at a time (independent loads) in a warp-uniform loop.
 // The tile's inclusive prefix is published the moment it is known.
-template <typename LB, bool WAIT_PREFETCH = true>
+template <typename LB>
 __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, LB* __restrict__ lb_cur,
                                                                  const LB* lbw, uint32_t mycount) {
     using W = LookbackWord<LB>;
@@ -691,7 +672,7 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, 
     bool done = false;
     const LB* col = lb_cur + tid;
     LB* mine = lb_cur + (size_t)tile * kRadix + tid;
-    if constexpr (WAIT_PREFETCH) asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
     bool stop = false;
 #pragma unroll
     for (int i = 0; i < PRE; ++i) {
@@ -740,12 +721,10 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, 
 // atomic are served in lane order, b2s::probe_lane_order), packed two per
 // word in `rr`. HOT: the pass's hot digit is ranked by one ballot per row
 // against a warp-uniform running count instead (same-address atomics
-// serialise). !FULL: only the warp's items below `valid` (tile-relative
-// index wbase + j * 32 + lane) count.
-template <typename U, int ITEMS, bool HOT, bool FULL = true>
+// serialise).
+template <typename U, int ITEMS, bool HOT>
 __device__ __forceinline__ void early_ranks(const U (&keys)[ITEMS], uint32_t (&rr)[(ITEMS + 1) / 2],
-                                            uint32_t* ecnt, int shift, uint32_t dxor, uint32_t hot,
-                                            uint32_t wbase = 0, uint32_t valid = 0) {
+                                            uint32_t* ecnt, int shift, uint32_t dxor, uint32_t hot) {
     const int lane = threadIdx.x & 31;
     {
         uint4* z = reinterpret_cast<uint4*>(ecnt);
@@ -765,18 +744,15 @@ __device__ __forceinline__ void early_ranks(const U (&keys)[ITEMS], uint32_t (&r
         for (int b = 0; b < B; ++b) {
             if (j0 + b < ITEMS) {
                 const uint32_t d = digit_of(keys[j0 + b], shift, dxor);
-                const bool v = FULL || wbase + (j0 + b) * 32 + lane < valid;
                 s16[b] = 16 * (d & 1);
                 if constexpr (HOT) {
-                    h[b] = v && d == hot;
+                    h[b] = d == hot;
                     const uint32_t hm = __ballot_sync(0xffffffffu, h[b]);
                     hr[b] = hot_run + __popc(hm & lt);
                     hot_run += __popc(hm);
-                    old[b] = atom_add_shared_if(v && !h[b], ecnt_a + 4 * (d >> 1), 1u << s16[b]);
-                } else if constexpr (FULL) {
-                    old[b] = atom_add_shared(ecnt_a + 4 * (d >> 1), 1u << s16[b]);
+                    old[b] = atom_add_shared_if(!h[b], ecnt_a + 4 * (d >> 1), 1u << s16[b]);
                 } else {
-                    old[b] = atom_add_shared_if(v, ecnt_a + 4 * (d >> 1), 1u << s16[b]);
+                    old[b] = atom_add_shared(ecnt_a + 4 * (d >> 1), 1u << s16[b]);
                 }
             }
         }
@@ -1447,394 +1423,6 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
 }
 
-// ---------------------------------------------------------------------------
-// Pipelined onesweep pass with bulk write-out: 4-byte keys, no payload, every
-// digit histogram from the all-digit prologue, 16-byte aligned buffers.
-//
-// A staged LSD pass on B200 is bound by shared-memory wavefronts, and a
-// quarter of them went to the write-out (staged re-read, per-key digit
-// offset lookup, scalar global stores). Here each digit run is staged at the
-// 16-byte phase of its global destination (S = G mod 4, at most 3 slots of
-// padding per digit) and leaves shared memory as one cp.async.bulk store (the
-// up-to-3 head and tail keys by scalar stores): nothing per key runs after
-// the scatter. The padding needs the run's global offset G -- the look-back
-// -- before the scatter, and a look-back issued right after the tile's own
-// aggregates stalls on predecessors that have not published yet (0.99 ms
-// per 2^28-key pass vs 0.61 with the wait ablated). So tiles are pipelined
-// one deep: iteration k counts and ranks tile k+1 and publishes its
-// aggregates, and only then resolves tile k's look-back (published one
-// iteration earlier, so its predecessors have resolved) and scatters and
-// stores tile k. Per iteration, with tile k in buffer b and tile k+1 landed
-// in buffer b^1:
-//   E  every warp ranks its keys of tile k+1 in-warp (early counts into
-//      cnt[b^1], lane-ordered atomics -> packed ranks rr_next)        [B1]
-//   D  warps 0-3 scan cnt[b^1] over warps (digit pairs), publish tile k+1's
-//      aggregates and tile starts; threads < 256 prefetch its look-back
-//   K  thread d < 256: tile k's look-back -> G_d (the last tile needs none:
-//      G = end of the digit's region - its count), S_d, folded into every
-//      warp's lookup word of cnt[b]; every warp re-reads tile k's keys [B2]
-//   S  scatter tile k to its phase-aligned staging                   [B3]
-//   W  thread d stores run d; its bulk reads complete                [B4]
-//      the next tile streams into buffer b
-// Buffer 0 stages upwards from its start into the 3-KB gap after it, buffer
-// 1 downwards from its end into the same gap; the two never stage at once.
-// Look-back words, tile order and tile size are those of onesweep_kernel, so
-// the structured-input twin (onesweep_kernel RANK 4) shares the region.
-template <int THREADS, int ITEMS>
-struct PipeSmem {
-    static constexpr int WARPS = THREADS / 32;
-    static constexpr int TILE = THREADS * ITEMS;
-    static constexpr size_t kCnt = (size_t)WARPS * (kRadix / 2) * 4;  // packed u16 pairs
-    static constexpr size_t kKeys = (size_t)TILE * 4;
-    static constexpr size_t kGap = 3 * kRadix * 4;
-    // cnt[2] | keys[0] | gap | keys[1]
-    static constexpr size_t bytes = 2 * kCnt + 2 * kKeys + kGap;
-    static_assert(TILE + 3 * kRadix < 65536, "packed 16-bit staging offsets");
-    static_assert(kKeys % 16 == 0, "TMA tile copies");
-};
-
-template <typename LB>
-struct PipeShared {
-    LB goff[kRadix];                  // the slot's global digit offsets
-    uint32_t start[2][kRadix];        // tile starts of the digits, per buffer
-    uint32_t wsum[kRadix / 64];       // digit section: per-warp sums
-    unsigned long long wsum64[kRadix / 32];
-    alignas(16) LB lbw[2][LookbackWord<LB>::kPrefetch * kRadix];  // look-back prefetch, per buffer
-    uint32_t tile[2];
-    alignas(8) unsigned long long mbar[2];
-#if B2S_PIPE_VEC
-    uint32_t run[kRadix];  // staged run of digit d: lo | hi << 16
-    LB roff[kRadix];       // its global index minus its staged slot
-#endif
-};
-
-template <typename LB, int THREADS, int ITEMS, int MINB, bool HOT>
-__global__ void __launch_bounds__(THREADS, MINB) onesweep_pipe_kernel(RadixPlan* __restrict__ plan, int slot,
-                                                                      uint64_t n, uint32_t ntiles,
-                                                                      LB* __restrict__ lb_cur,
-                                                                      LB* __restrict__ lb_next,
-                                                                      uint64_t skew_limit) {
-    using U = uint32_t;
-    using SM = PipeSmem<THREADS, ITEMS>;
-    using W = LookbackWord<LB>;
-    constexpr int TILE = SM::TILE;
-    constexpr int WARPS = SM::WARPS;
-    constexpr int HALF = kRadix / 2;
-    constexpr int WSEG = 32 * ITEMS;
-    constexpr int PRE = W::kPrefetch;
-    constexpr int RR = (ITEMS + 1) / 2;
-    static_assert(THREADS >= kRadix, "one thread per digit");
-    // launched like onesweep_kernel RANK 2 (regular) / RANK 3 (skewed twin):
-    // the twins are programmatic dependents and exactly one kernel runs
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int na = plan->num_active;
-    if (slot >= na) return;
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    unsigned long long c = 0;  // this thread's digit count of the pass
-    if (tid < kRadix) c = plan->hist[slot][tid];
-    {
-        const bool skewed = __syncthreads_or(tid < kRadix && c > skew_limit) != 0;
-        const int mode = skewed ? 3 : (plan->structured ? 4 : 2);
-        if (mode != (HOT ? 3 : 2)) return;
-    }
-    uint32_t hot = 0;
-    if constexpr (HOT) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        __shared__ unsigned long long s_hot;
-        if (tid == 0) s_hot = 0;
-        __syncthreads();
-        if (tid < kRadix) atomicMax(&s_hot, (c << 8) | (unsigned long long)tid);
-        __syncthreads();
-        hot = (uint32_t)(s_hot & 0xFF);
-    }
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ PipeShared<LB> sh;
-    uint32_t* const cnt_base = reinterpret_cast<uint32_t*>(smem);
-    U* const kb0 = reinterpret_cast<U*>(smem + 2 * SM::kCnt);
-    auto cntb = [&](int b) { return cnt_base + (b ? WARPS * HALF : 0); };
-    auto kbuf = [&](int b) { return kb0 + (b ? TILE + 3 * kRadix : 0); };
-    auto kstage = [&](int b) { return kb0 + (b ? TILE : 0); };
-
-    const int shift = 8 * plan->digit[slot];
-    const uint32_t dxor = plan->dxor[slot];
-    const U* __restrict__ src = static_cast<const U*>(plan->ksrc[slot]);
-    U* __restrict__ dst = static_cast<U*>(plan->kdst[slot]);
-    // 16-byte phase of the destination array in keys (it is 16-byte aligned
-    // when launched, kept general)
-    const uint32_t dph = (uint32_t)(reinterpret_cast<uintptr_t>(dst) >> 2);
-    const uint32_t mbar_a[2] = {smem_addr(&sh.mbar[0]), smem_addr(&sh.mbar[1])};
-    const uint32_t wbase = warp * WSEG;
-    auto valid_of = [&](uint32_t t) -> uint32_t {
-        const uint64_t rem = n - (uint64_t)t * TILE;
-        return rem >= (uint64_t)TILE ? (uint32_t)TILE : (uint32_t)rem;
-    };
-    auto prefetch = [&](uint32_t t, int b) {  // one thread; full tiles only
-        if (t < ntiles && valid_of(t) == (uint32_t)TILE) {
-            fence_proxy_async();
-            mbar_expect_tx(mbar_a[b], (uint32_t)SM::kKeys);
-            bulk_g2s(smem_addr(kbuf(b)), src + (uint64_t)t * TILE, (uint32_t)SM::kKeys, mbar_a[b]);
-        }
-    };
-
-    // global digit offsets of this slot: exclusive scan of its histogram
-    if (tid < kRadix) {
-        unsigned long long incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) sh.wsum64[tid >> 5] = incl;
-        sh.goff[tid] = (LB)(incl - c);
-    }
-    if (tid == THREADS - 1) {
-        mbar_init(mbar_a[0], 1);
-        mbar_init(mbar_a[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t t0 = atomicAdd(&plan->tile_counter[slot], 1u);
-        const uint32_t t1 = atomicAdd(&plan->tile_counter[slot], 1u);
-        sh.tile[0] = t0;
-        sh.tile[1] = t1;
-        prefetch(t0, 0);
-        prefetch(t1, 1);
-    }
-    __syncthreads();
-    if (tid < kRadix) {
-        unsigned long long base = 0;
-#pragma unroll
-        for (int w = 0; w < kRadix / 32; ++w) base += (w < (tid >> 5)) ? sh.wsum64[w] : 0ull;
-        sh.goff[tid] += (LB)base;
-    }
-    uint32_t parity = 0;  // bit b: phase parity of buffer b's mbarrier
-    unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long prof_t = clock64();
-    (void)prof_t;
-
-    // ---- E: keys of tile t (buffer b) -> in-warp ranks, early counts in cnt[b]
-    auto rank_tile = [&](uint32_t t, int b, uint32_t (&rr)[RR]) {
-        U keys[ITEMS];
-        const uint32_t valid = valid_of(t);
-        if (valid == (uint32_t)TILE) {
-            mbar_wait(mbar_a[b], (parity >> b) & 1u);
-            parity ^= 1u << b;
-            B2S_PHASE(0);
-            const U* kb = kbuf(b);
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) keys[j] = kb[wbase + j * 32 + lane];
-            early_ranks<U, ITEMS, HOT>(keys, rr, cntb(b) + warp * HALF, shift, dxor, hot);
-        } else {
-            const U* s = src + (uint64_t)t * TILE + wbase + lane;
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) keys[j] = (wbase + j * 32 + lane < valid) ? s[j * 32] : 0u;
-            early_ranks<U, ITEMS, HOT, false>(keys, rr, cntb(b) + warp * HALF, shift, dxor, hot, wbase, valid);
-        }
-    };
-    // ---- D: warps 0-3 (thread t owns digits 2t, 2t+1): per-warp exclusive
-    // prefixes in cnt[b], the tile's aggregates, the tile starts
-    auto digit_section = [&](uint32_t t, int b) {
-        if (tid < HALF) {
-            uint32_t* cnt = cntb(b);
-            uint32_t pair = 0;
-#pragma unroll 4
-            for (int w = 0; w < WARPS; ++w) {
-                const uint32_t v = cnt[w * HALF + tid];
-                cnt[w * HALF + tid] = pair;
-                pair += v;
-            }
-            const uint32_t c0 = pair & 0xFFFFu, c1 = pair >> 16;
-            if (t + 1 < ntiles) {  // the last tile has no successor
-                LB* slotw = lb_cur + (size_t)t * kRadix + 2 * tid;
-                const LB flag = t == 0 ? W::kInc : W::kAgg;
-                st_relaxed(slotw, flag | (LB)c0);
-                st_relaxed(slotw + 1, flag | (LB)c1);
-            }
-            uint32_t incl = c0 + c1;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            if (lane == 31) sh.wsum[warp] = incl;
-            asm volatile("bar.sync 1, %0;" ::"n"(HALF) : "memory");
-            uint32_t base = 0;
-#pragma unroll
-            for (int w = 0; w < HALF / 32; ++w) base += (w < warp) ? sh.wsum[w] : 0u;
-            sh.start[b][2 * tid] = base + incl - c0 - c1;
-            sh.start[b][2 * tid + 1] = base + incl - c1;
-        }
-    };
-    // look-back prefetch of tile t's first predecessors (one cp.async group
-    // per tile, possibly empty)
-    auto lb_prefetch = [&](uint32_t t, int b) {
-        if (tid < kRadix) {
-            if (t > 0 && t + 1 < ntiles) {
-#pragma unroll
-                for (int i = 0; i < PRE; ++i) {
-                    if ((int64_t)t - 1 - i >= 0)
-                        cp_async_lb(smem_addr(&sh.lbw[b][i * kRadix + tid]), lb_cur + (size_t)(t - 1 - i) * kRadix + tid);
-                }
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-    };
-
-    // prime the pipeline with the first tile
-    uint32_t cur = sh.tile[0];
-    int bc = 0;
-    uint32_t rr_cur[RR];
-    if (cur < ntiles) {
-        rank_tile(cur, 0, rr_cur);
-        lb_prefetch(cur, 0);
-    }
-    __syncthreads();
-    if (cur < ntiles) digit_section(cur, 0);
-
-    while (cur < ntiles) {
-        const uint32_t nxt = sh.tile[bc ^ 1];
-        const bool has_next = nxt < ntiles;
-        const uint32_t cur_valid = valid_of(cur);
-        uint32_t nn = 0;
-        if (tid == THREADS - 1) {
-            nn = atomicAdd(&plan->tile_counter[slot], 1u);
-            sh.tile[bc] = nn;  // cur's id is in every thread's register
-        }
-        if (tid < kRadix) lb_next[(size_t)cur * kRadix + tid] = 0;  // the next pass's look-back words
-
-        // ---- E(next)
-        uint32_t rr_next[RR];
-        if (has_next) {
-            rank_tile(nxt, bc ^ 1, rr_next);
-            lb_prefetch(nxt, bc ^ 1);
-        }
-        B2S_PHASE(1);
-        __syncthreads();  // B1: cnt[b^1] complete; sh.start[bc] (previous iteration) visible
-        B2S_PHASE(2);
-        // ---- D(next)
-        if (has_next) digit_section(nxt, bc ^ 1);
-        B2S_PHASE(3);
-        // ---- K(cur)
-        LB g = 0;
-        uint32_t s = 0, cnt = 0;
-        if (tid < kRadix) {
-            if (has_next) asm volatile("cp.async.wait_group 1;" ::: "memory");
-            else asm volatile("cp.async.wait_group 0;" ::: "memory");
-            const uint32_t st = sh.start[bc][tid];
-            cnt = (tid + 1 < kRadix ? sh.start[bc][tid + 1] : cur_valid) - st;
-            unsigned long long excl;
-            if (cur + 1 == ntiles) excl = c - cnt;  // the last tile ends each digit's region
-#ifdef B2S_ABL_NOLB
-            else excl = (unsigned long long)cur * TILE + st - sh.goff[tid];  // ablation: in bounds, wrong order
-#else
-            else excl = lookback_exclusive<LB, false>(cur, lb_cur, sh.lbw[bc], cnt);
-#endif
-            g = (LB)(sh.goff[tid] + excl);
-            // staged run start: at least 3 slots per digit before it, same
-            // 16-byte phase as its destination address
-            s = st + 3u * tid + (dph + (uint32_t)g - st - 3u * tid) % 4u;
-            const uint32_t so = __shfl_xor_sync(0xffffffffu, s, 1);
-            const uint32_t add = (tid & 1) ? (so | (s << 16)) : (s | (so << 16));
-            // each pair's words: the even digit's thread updates the first
-            // half of the warps, the odd one the second
-            uint32_t* cw = cntb(bc) + (tid >> 1);
-            const int w0 = (tid & 1) * (WARPS / 2);
-#pragma unroll
-            for (int w = w0; w < w0 + WARPS / 2; ++w) cw[w * HALF] += add;
-#if B2S_PIPE_VEC
-            sh.run[tid] = s | ((s + cnt) << 16);
-            sh.roff[tid] = (LB)(g - (LB)s);
-#endif
-        }
-        B2S_PHASE(4);
-        // ---- S(cur): re-read the keys, scatter them in place
-        U keys[ITEMS];
-        if (cur_valid == (uint32_t)TILE) {
-            const U* kb = kbuf(bc);
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) keys[j] = kb[wbase + j * 32 + lane];
-        } else {
-            const U* sp = src + (uint64_t)cur * TILE + wbase + lane;
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) keys[j] = (wbase + j * 32 + lane < cur_valid) ? sp[j * 32] : 0u;
-        }
-        __syncthreads();  // B2: lookup words final, every key read
-        B2S_PHASE(5);
-        {
-            const uint32_t* wc = cntb(bc) + warp * HALF;
-            const uint32_t stage_a = smem_addr(kstage(bc));
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                if (cur_valid == (uint32_t)TILE || wbase + j * 32 + lane < cur_valid) {
-                    const uint32_t d = digit_of(keys[j], shift, dxor);
-                    const uint32_t r = ((wc[d >> 1] >> (16 * (d & 1))) & 0xFFFFu) +
-                                       ((rr_cur[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
-                    sts_key(stage_a + 4 * r, keys[j]);
-                }
-            }
-        }
-        fence_proxy_async();  // the staged keys are visible to the bulk copies
-        __syncthreads();      // B3
-        B2S_PHASE(6);
-#if B2S_PIPE_VEC
-        // ---- W(cur): 16-byte chunks of the staging; a chunk inside one run
-        // is one 16-byte store (its staged and global phases agree), others
-        // go key by key (padding slots belong to no run)
-        {
-            const uint4* st4 = reinterpret_cast<const uint4*>(kstage(bc));
-            constexpr int NCH = (TILE + 3 * kRadix) / 4;
-            for (int q = tid; q < NCH; q += THREADS) {
-                const uint4 v = st4[q];
-                const uint32_t i0 = 4u * q;
-                const uint32_t d0 = digit_of(v.x, shift, dxor), d3 = digit_of(v.w, shift, dxor);
-                const uint32_t r0 = sh.run[d0];
-                if (d0 == d3 && i0 >= (r0 & 0xFFFFu) && i0 + 4 <= (r0 >> 16)) {
-                    __stcs(reinterpret_cast<uint4*>(dst + (LB)(sh.roff[d0] + i0)), v);
-                } else {
-                    const uint32_t e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint32_t d = digit_of(e[k], shift, dxor);
-                        const uint32_t r = sh.run[d];
-                        if (i0 + k >= (r & 0xFFFFu) && i0 + k < (r >> 16)) __stcs(dst + (LB)(sh.roff[d] + i0 + k), e[k]);
-                    }
-                }
-            }
-        }
-        (void)g;
-        (void)s;
-        (void)cnt;
-#else
-        // ---- W(cur): thread d stores run d
-        if (tid < kRadix) {
-            if (cnt) {
-                const U* stg = kstage(bc);
-                const uint32_t head = min(cnt, (0u - dph - (uint32_t)g) % 4u);
-                const uint32_t body = (cnt - head) & ~3u;
-                for (uint32_t i = 0; i < head; ++i) __stcs(dst + g + i, stg[s + i]);
-                if (body) bulk_s2g(dst + g + head, smem_addr(stg + s + head), body * 4u);
-                for (uint32_t i = head + body; i < cnt; ++i) __stcs(dst + g + i, stg[s + i]);
-            }
-            bulk_commit();
-            bulk_wait_read0();
-        }
-#endif
-        __syncthreads();  // B4: buffer bc is free
-        if (tid == THREADS - 1) prefetch(nn, bc);
-        B2S_PHASE(7);
-#pragma unroll
-        for (int i = 0; i < RR; ++i) rr_cur[i] = rr_next[i];
-        cur = has_next ? nxt : ntiles;
-        bc ^= 1;
-    }
-    if (tid < kRadix) bulk_wait0();  // the bulk stores are complete before the grid ends
-#ifdef B2S_PHASE_PROFILE
-    if (tid == 0 || tid == THREADS - 1)
-        for (int q = 0; q < 8; ++q) atomicAdd(&b2s_phase_cycles[tid == 0 ? 0 : 1][q], prof_acc[q]);
-#endif
-}
-
 template <typename U>
 __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n, int with_vals) {
     if (!plan->do_copy) return;
@@ -1876,63 +1464,34 @@ uint64_t skew_limit(uint64_t n) {
     return sh >= 64 ? ~0ull : (n >> sh);
 }
 
-// Pipelined bulk-store kernels (regular, skewed) exist for 4-byte keys
-// without payload in the default tile configuration.
-template <typename U, bool VALS, int THREADS, int ITEMS, int MINB>
-constexpr bool kHasPipe = sizeof(U) == 4 && !VALS && THREADS == 512 && ITEMS == B2S_U32_ITEMS && MINB == 2;
-
-// B2S_PIPE=0 keeps every pass on onesweep_kernel (for A/B measurements)
-bool pipe_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("B2S_PIPE");
-        v = e ? atoi(e) : 0;  // experiment: 0.88 ms per 2^28-key u32 pass vs 0.70 for onesweep_kernel
-    }
-    return v != 0;
-}
-
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB, int RANK>
 b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
-                               void* lb, bool pipe) {
+                               void* lb) {
     using SM = OnesweepSmem<U, VALS, THREADS, ITEMS>;
     constexpr int TILE = SM::TILE;
+    constexpr size_t SMEM = SM::bytes;
     // the regular kernel and, for RANK 2, its skewed-pass and structured-input
-    // twins (same tile, so the same look-back layout). With `pipe` (all-digit
-    // prologue, 16-byte aligned buffers) the regular and skewed kernels are
-    // the pipelined bulk-store ones.
+    // twins (same tile and shared memory, so the same look-back layout)
     using Kern = void (*)(RadixPlan*, RadixCounters*, int, uint64_t, uint32_t, LB*, LB*, uint64_t);
-    using PKern = void (*)(RadixPlan*, int, uint64_t, uint32_t, LB*, LB*, uint64_t);
-    constexpr bool HAS_PIPE = RANK == 2 && kHasPipe<U, VALS, THREADS, ITEMS, MINB>;
-    pipe = pipe && HAS_PIPE && pipe_enabled();
     constexpr int NK = RANK == 2 ? 3 : 1;
     const Kern kern[3] = {onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, RANK>,
                           onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 3>,
                           onesweep_kernel<U, VALS, LB, THREADS, ITEMS, MINB, 4>};
-    PKern pkern[2] = {nullptr, nullptr};
-    if constexpr (HAS_PIPE) {
-        pkern[0] = onesweep_pipe_kernel<LB, THREADS, ITEMS, MINB, false>;
-        pkern[1] = onesweep_pipe_kernel<LB, THREADS, ITEMS, MINB, true>;
-    }
-    constexpr size_t SMEM = SM::bytes;
-    constexpr size_t PSMEM = PipeSmem<THREADS, ITEMS>::bytes;
     static int occ[3] = {-1, -1, -1};  // per instantiation (one device type)
-    static int pocc[2] = {-1, -1};
     static DeviceOnce once;
     B2S_TRY(once_per_device(once, ctx->device, [&]() -> b2s_status {
-        for (int k = 0; k < NK + (HAS_PIPE ? 2 : 0); ++k) {
-            const bool pk = k >= NK;
-            const void* f = pk ? (const void*)pkern[k - NK] : (const void*)kern[k];
-            const size_t sm = pk ? PSMEM : SMEM;
-            B2S_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        for (int k = 0; k < NK; ++k) {
+            B2S_CUDA(cudaFuncSetAttribute(kern[k], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)SMEM));
             int o = 0;
-            B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, THREADS, sm));
-            (pk ? pocc[k - NK] : occ[k]) = o > 0 ? o : 1;
+            B2S_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern[k], THREADS, SMEM));
+            occ[k] = o > 0 ? o : 1;
             if (getenv("B2S_DEBUG")) {
                 cudaFuncAttributes fa;
-                cudaFuncGetAttributes(&fa, f);
-                fprintf(stderr, "[b2s] onesweep%s<%zuB keys, vals=%d, %d thr, %d items, rank=%d>: dyn smem %zu + static %zu B, regs %d, %d CTA/SM\n",
-                        pk ? "_pipe" : "", sizeof(U), (int)VALS, THREADS, ITEMS,
-                        pk ? k - NK + 2 : (k == 0 ? RANK : k + 2), sm, (size_t)fa.sharedSizeBytes, fa.numRegs, o);
+                cudaFuncGetAttributes(&fa, kern[k]);
+                fprintf(stderr, "[b2s] onesweep<%zuB keys, vals=%d, %d thr, %d items, rank=%d>: dyn smem %zu + static %zu B, regs %d, %d CTA/SM\n",
+                        sizeof(U), (int)VALS, THREADS, ITEMS, k == 0 ? RANK : k + 2, (size_t)SMEM,
+                        (size_t)fa.sharedSizeBytes, fa.numRegs, occ[k]);
             }
         }
         return B2S_OK;
@@ -1955,15 +1514,8 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
             at[0].val.programmaticStreamSerializationAllowed = 1;
             lc.attrs = at;
             lc.numAttrs = k > 0 ? 1 : 0;  // the twins are programmatic dependents
-            if (pipe && k < 2) {
-                lc.gridDim = dim3((uint32_t)std::min<uint64_t>(ntiles64, (uint64_t)pocc[k] * ctx->num_sms));
-                lc.dynamicSmemBytes = PSMEM;
-                B2S_CUDA(cudaLaunchKernelEx(&lc, pkern[k], plan, s, n, ntiles, region[s & 1], region[(s + 1) & 1],
-                                            skew));
-            } else {
-                B2S_CUDA(cudaLaunchKernelEx(&lc, kern[k], plan, ctr, s, n, ntiles, region[s & 1],
-                                            region[(s + 1) & 1], skew));
-            }
+            B2S_CUDA(cudaLaunchKernelEx(&lc, kern[k], plan, ctr, s, n, ntiles, region[s & 1],
+                                        region[(s + 1) & 1], skew));
             note_launch();
         }
     }
@@ -1973,14 +1525,14 @@ b2s_status launch_passes_cfg_r(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr
 
 template <typename U, bool VALS, typename LB, int THREADS, int ITEMS, int MINB>
 b2s_status launch_passes_cfg(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n,
-                             void* lb, bool pipe) {
+                             void* lb) {
     // small sorts are bound by the chain of dependent launches, not by the
     // ranking: one kernel per pass (no skewed / structured twins)
     if (ctx->atomic_rank && n < kTwinMinKeys)
-        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb, false);
+        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 1>(ctx, plan, ctr, n, lb);
     if (ctx->atomic_rank)
-        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 2>(ctx, plan, ctr, n, lb, pipe);
-    return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb, false);
+        return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 2>(ctx, plan, ctr, n, lb);
+    return launch_passes_cfg_r<U, VALS, LB, THREADS, ITEMS, MINB, 0>(ctx, plan, ctr, n, lb);
 }
 
 // Tile configuration of a sort: threads x items per CTA, CTAs per SM
@@ -2009,22 +1561,19 @@ TileCfg tile_cfg(int kbytes, bool vals, uint64_t n) {
 }
 
 template <typename U, bool VALS, typename LB>
-b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb,
-                         bool pipe) {
+b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint64_t n, void* lb) {
     const TileCfg c = tile_cfg((int)sizeof(U), VALS, n);
     if constexpr (sizeof(U) == 4 && VALS) {
-        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb, pipe);
+        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
-        if (c.items == 16) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb, pipe);
-        return launch_passes_cfg<U, VALS, LB, 512, B2S_U32_ITEMS, 2>(ctx, plan, ctr, n, lb, pipe);
+        if (c.items == 16) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, 512, B2S_U32_ITEMS, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
-        return launch_passes_cfg<U, VALS, LB, 1024, 8, 1>(ctx, plan, ctr, n, lb, pipe);
+        return launch_passes_cfg<U, VALS, LB, 1024, 8, 1>(ctx, plan, ctr, n, lb);
     } else {
-        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb, pipe);
+        return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     }
 }
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <typename U, bool VALS>
 b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kout,
@@ -2089,14 +1638,10 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     ctx->last_passes_possible = NP;
 
     if (n > 0) {
-        // the pipelined bulk-store passes need every digit histogram up front
-        // (no in-pass counting) and 16-byte aligned key buffers (TMA and bulk
-        // copies on every slot of the ping-pong chain)
-        const bool pipe = all_hist && aligned16(kin) && aligned16(kout) && aligned16(sc->alt_keys);
         if (wide)
-            B2S_TRY((launch_passes<U, VALS, unsigned long long>(ctx, plan, ctr, n, sc->lookback, pipe)));
+            B2S_TRY((launch_passes<U, VALS, unsigned long long>(ctx, plan, ctr, n, sc->lookback)));
         else
-            B2S_TRY((launch_passes<U, VALS, uint32_t>(ctx, plan, ctr, n, sc->lookback, pipe)));
+            B2S_TRY((launch_passes<U, VALS, uint32_t>(ctx, plan, ctr, n, sc->lookback)));
     }
     {
         int grid = (int)std::min<uint64_t>(std::max<uint64_t>((n + 1023) / 1024, 1),
