@@ -300,10 +300,18 @@ b2s_status merge2_window(b2s_ctx* ctx, const T* a, const uint32_t* va, uint64_t 
 constexpr int kMaxK = 16;
 constexpr int kKThreads = 256;
 
+#ifndef B2S_KG_CAP
+#define B2S_KG_CAP 8192  // records per group (4-byte keys): 256 threads x 33 items, two CTAs per SM
+#endif
+#ifndef B2S_KG_ITEMS
+#define B2S_KG_ITEMS 33
+#endif
 template <typename T>
 struct GroupCfg {
-    static constexpr uint32_t S = sizeof(T) == 4 ? 256 : 128;   // sample stride
-    static constexpr uint32_t T_ = sizeof(T) == 4 ? 4096 : 2048; // group target
+    static constexpr uint32_t S = sizeof(T) == 4 ? 256 : 128;              // sample stride
+    static constexpr uint32_t CAP = sizeof(T) == 4 ? B2S_KG_CAP : 3200;    // records a group may hold
+    // group target: with k runs a group then holds at most CAP records
+    static constexpr uint32_t target(int k) { return CAP - (uint32_t)k * S; }
 };
 
 template <typename T>
@@ -369,76 +377,155 @@ __global__ void kmerge_cuts_kernel(const KRuns<T> R, const T* __restrict__ skeys
 }
 
 // shared bytes of a group kernel for k runs: two buffers of cap records. The
-// first buffer holds the k slices each at its global 16-byte phase (up to
-// 2V-2 records of padding per slice), the output is restaged at its phase,
-// and the merge may read one record past the end.
+// first buffer holds the k key slices each at its global 16-byte phase (up to
+// V-1 records of padding per slice; the payload slices sit at the same
+// indices of the value buffer), the output is restaged at its phase, and the
+// merge reads one record past the end of a segment.
 template <typename T, bool VALS>
 constexpr uint32_t group_cap(int k) {
-    return (GroupCfg<T>::T_ + (uint32_t)k * GroupCfg<T>::S + (uint32_t)(2 * k + 2) * 4 + 4 + 3) / 4 * 4;
+    return (GroupCfg<T>::CAP + (uint32_t)(2 * k + 2) * 4 + 4 + 3) / 4 * 4;
 }
 template <typename T, bool VALS>
 constexpr size_t group_smem(uint32_t cap) {
     return 2 * (size_t)cap * sizeof(T) + (VALS ? 2 * (size_t)cap * 4 : 0);
 }
 
-// One group: its k slices are staged in shared memory with 16-byte copies
-// (each at its global phase, so the first round reads segments with gaps),
-// merged pairwise in shared memory (log2 k rounds, ties to the lower run,
-// two heads in registers; the last round writes at the output's phase) and
-// written with 16-byte stores.
+// outputs per thread and merge round (odd: a warp's per-round output stores,
+// ITEMS records apart, hit distinct banks)
+template <typename T>
+struct GroupItems {
+    static constexpr int value = sizeof(T) == 4 ? B2S_KG_ITEMS : 13;
+};
+
+template <typename T>
+__device__ __forceinline__ T lds_rec(uint32_t a) {
+    if constexpr (sizeof(T) == 4) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+        return (T)v;
+    } else {
+        unsigned long long v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+        return (T)v;
+    }
+}
+template <typename T>
+__device__ __forceinline__ void sts_rec(uint32_t a, T v) {
+    if constexpr (sizeof(T) == 4)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"((uint32_t)v) : "memory");
+    else
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"((unsigned long long)v) : "memory");
+}
+
+// Merge path on shared-memory segments given by byte address: the number of
+// A records among the first `diag` outputs (ties to A).
+template <typename T>
+__device__ __forceinline__ uint32_t merge_path_sa(uint32_t a, uint32_t na, uint32_t b, uint32_t nb,
+                                                  uint32_t diag) {
+    uint32_t lo = diag > nb ? diag - nb : 0;
+    uint32_t hi = diag < na ? diag : na;
+    const uint32_t bd = b + (diag - 1) * (uint32_t)sizeof(T);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const bool a_first = !(lds_rec<T>(bd - mid * (uint32_t)sizeof(T)) < lds_rec<T>(a + mid * (uint32_t)sizeof(T)));
+        lo = a_first ? mid + 1 : lo;
+        hi = a_first ? hi : mid;
+    }
+    return lo;
+}
+
+// One group: its k slices are staged in shared memory (keys by 16-byte
+// copies at their global phase, payloads element-wise at the same indices),
+// merged pairwise in shared memory (ceil(log2 k) rounds, ties to the lower
+// run; the last round writes at the output's 16-byte phase) and written with
+// 16-byte stores. The merge step keeps both heads and both read positions
+// (shared byte addresses) in registers: per output one compare, one store,
+// one load of the taken side's next record and selects -- no index
+// arithmetic. (The first version, index-based, issued 147 instructions per
+// output for k = 8.)
 template <typename T, bool VALS>
 __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> R,
                                                                  const uint64_t* __restrict__ cuts,
                                                                  uint32_t cap, T* __restrict__ out,
                                                                  uint32_t* __restrict__ vout) {
-    constexpr int ITEMS = sizeof(T) == 4 ? 19 : 15;  // odd: conflict-free strided stores
+    constexpr int ITEMS = GroupItems<T>::value;
     constexpr uint32_t V = 16 / sizeof(T);
+    constexpr uint32_t SZ = sizeof(T);
     extern __shared__ __align__(16) unsigned char smem[];
-    // buffers are selected arithmetically (an indexed pointer array would
-    // lose the shared address space and turn every access generic)
     T* const kbase = reinterpret_cast<T*>(smem);
     uint32_t* const vbase = reinterpret_cast<uint32_t*>(smem + 2 * (size_t)cap * sizeof(T));
-    __shared__ uint32_t s_seg[kMaxK + 1];          // output-space segments (prefix of lengths)
-    __shared__ uint32_t s_kbeg[kMaxK], s_vbeg[kMaxK];  // staged slices in buffer 0
+    __shared__ uint32_t s_seg[kMaxK + 1];  // output-space segments (prefix of lengths)
+    __shared__ uint32_t s_kbeg[kMaxK];     // staged slices in buffer 0 (record index)
     __shared__ uint64_t s_lo[kMaxK];
     __shared__ uint64_t s_out;
     const int k = R.k;
     const int tid = threadIdx.x;
     const uint64_t g = blockIdx.x;
-    if (tid == 0) {
-        uint32_t acc = 0, kp = 0, vp = 0;
-        uint64_t o = 0;
-        for (int r = 0; r < k; ++r) {
-            const uint64_t lo = cuts[g * k + r], hi = cuts[(g + 1) * k + r];
-            const uint32_t len = (uint32_t)(hi - lo);
-            s_lo[r] = lo;
-            s_seg[r] = acc;
-            kp = (kp + V - 1) / V * V + phase16(R.key[r] + lo);
-            s_kbeg[r] = kp;
-            kp += len;
-            if constexpr (VALS) {
-                vp = (vp + 3) / 4 * 4 + phase16(R.val[r] + lo);
-                s_vbeg[r] = vp;
-                vp += len;
-            }
-            acc += len;
-            o += lo;
+    if (tid < 32) {
+        // lane r < k: run r's slice [lo, hi) of this group; its staged slot
+        // spans roundup(phase + len, V) records, the keys start at its phase
+        uint64_t lo = 0;
+        uint32_t len = 0, ph = 0;
+        if (tid < k) {
+            lo = cuts[g * k + tid];
+            len = (uint32_t)(cuts[(g + 1) * k + tid] - lo);
+            ph = phase16(R.key[tid] + lo);
         }
-        s_seg[k] = acc;
-        s_out = o;
+        uint32_t acc = len, slot = (ph + len + V - 1) / V * V;
+        uint64_t o = lo;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t a2 = __shfl_up_sync(0xffffffffu, acc, d);
+            const uint32_t s2 = __shfl_up_sync(0xffffffffu, slot, d);
+            if (tid >= d) {
+                acc += a2;
+                slot += s2;
+            }
+            o += __shfl_xor_sync(0xffffffffu, o, d);
+        }
+        if (tid < k) {
+            s_lo[tid] = lo;
+            s_seg[tid + 1] = acc;
+            s_kbeg[tid] = slot - (ph + len + V - 1) / V * V + ph;
+        }
+        if (tid == 0) {
+            s_seg[0] = 0;
+            s_out = o;
+        }
     }
     __syncthreads();
     const uint32_t total = s_seg[k];
-    for (int r = 0; r < k; ++r) {
-        const uint32_t len = s_seg[r + 1] - s_seg[r];
-        stage_slice(kbase + s_kbeg[r], R.key[r] + s_lo[r], len);
-        if constexpr (VALS) stage_slice(vbase + s_vbeg[r], R.val[r] + s_lo[r], len);
+    // warp w stages runs w, w + 8, ...: 16-byte copies of the aligned middle,
+    // single records for the head and tail
+    {
+        const int lane = tid & 31;
+        for (int r = tid >> 5; r < k; r += kKThreads / 32) {
+            const uint32_t len = s_seg[r + 1] - s_seg[r];
+            T* sd = kbase + s_kbeg[r];
+            const T* src = R.key[r] + s_lo[r];
+            const uint32_t head = min((V - phase16(src)) % V, len);
+            const uint32_t nv = (len - head) / V;
+            const uint32_t tail0 = head + nv * V;
+            for (uint32_t v = lane; v < nv; v += 32) cp_async_16(sd + head + v * V, src + head + v * V);
+            if ((uint32_t)lane < head) cp_async_elem(sd + lane, src + lane);
+            else if ((uint32_t)lane >= V && lane - V < len - tail0)
+                cp_async_elem(sd + tail0 + (lane - V), src + tail0 + (lane - V));
+            if constexpr (VALS) {
+                const uint32_t* vs = R.val[r] + s_lo[r];
+                for (uint32_t i = lane; i < len; i += 32) cp_async_elem(vbase + s_kbeg[r] + i, vs + i);
+            }
+        }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const uint64_t o = s_out;
     const uint32_t po = phase16(out + o);
-    const uint32_t pvo = VALS ? phase16(vout + o) : 0u;
+    const uint32_t k0 = (uint32_t)__cvta_generic_to_shared(kbase);
+    const uint32_t v0 = (uint32_t)__cvta_generic_to_shared(vbase);
+    // payload address of the record at key address a (same record index)
+    auto vaddr = [&](uint32_t a) -> uint32_t {
+        return sizeof(T) == 4 ? a + (v0 - k0) : v0 + ((a - k0) >> 1);
+    };
     // pairwise rounds in shared memory; after a round segment i spans the old
     // segments 2i and 2i+1
     int cur = 0;
@@ -446,51 +533,56 @@ __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> 
     bool first = true;
     while (m > 1) {
         const bool last = (m + 1) / 2 == 1;
-        const T* ks = kbase + (cur ? cap : 0);
-        T* kd = kbase + (cur ? 0 : cap) + (last ? po : 0);
-        const uint32_t* vs = vbase + (cur ? cap : 0);
-        uint32_t* vd = vbase + (cur ? 0 : cap) + (last ? pvo : 0);
-        for (uint32_t x0 = tid * ITEMS; x0 < total; x0 += kKThreads * ITEMS) {
-            const uint32_t x1 = min(x0 + ITEMS, total);
-            uint32_t x = x0;
+        const uint32_t ks = k0 + (cur ? cap * SZ : 0u);
+        const uint32_t kd = k0 + (cur ? 0u : cap * SZ) + (last ? po * SZ : 0u);
+        // chunks of ITEMS outputs never straddle a pair: pair p owns chunks
+        // [c(p), c(p+1)) with c(p) = sum of ceil(len / ITEMS) below it
+        const int npairs = (m + 1) / 2;
+        uint32_t nchunks = 0;
+        for (int q = 0; q < npairs; ++q) nchunks += (s_seg[min(2 * q + 2, m)] - s_seg[2 * q] + ITEMS - 1) / ITEMS;
+        for (uint32_t c = tid; c < nchunks; c += kKThreads) {
             int p = 0;
-            while (2 * (p + 1) < m && s_seg[2 * (p + 1)] <= x) ++p;  // pair holding x
-            while (x < x1) {
-                // pair p: A = segment 2p, B = segment 2p+1 (empty past the end)
-                const int ia = 2 * p, ib = min(2 * p + 1, m);
-                const uint32_t o0 = s_seg[ia];
-                const uint32_t la = s_seg[min(ia + 1, m)] - o0;
-                const uint32_t lb = s_seg[min(ib + 1, m)] - s_seg[ib];
-                const T* ka_p = ks + (first ? s_kbeg[ia] : o0);
-                const T* kb_p = ks + (first ? (ib < m ? s_kbeg[ib] : 0u) : s_seg[ib]);
-                const uint32_t* va_p = vs + (VALS ? (first ? s_vbeg[ia] : o0) : 0u);
-                const uint32_t* vb_p = vs + (VALS ? (first ? (ib < m ? s_vbeg[ib] : 0u) : s_seg[ib]) : 0u);
-                const uint32_t diag = x - o0;
-                uint32_t ai = merge_path_smem(ka_p, la, kb_p, lb, diag);
-                uint32_t bi = diag - ai;
-                T ka = ka_p[ai], kb = kb_p[bi];
-                const uint32_t stop = min(x1, o0 + la + lb);
-                if (x == x0 && stop == x0 + ITEMS) {
-                    // common case: the whole chunk inside one pair, unrolled
-#pragma unroll
-                    for (int j = 0; j < ITEMS; ++j) {
-                        const bool take_a = bi >= lb || (ai < la && !(kb < ka));
-                        kd[x0 + j] = take_a ? ka : kb;
-                        if constexpr (VALS) vd[x0 + j] = take_a ? va_p[ai] : vb_p[bi];
-                        if (take_a) ka = ka_p[++ai];
-                        else kb = kb_p[++bi];
-                    }
-                    x = x1;
-                } else {
-                    for (; x < stop; ++x) {
-                        const bool take_a = bi >= lb || (ai < la && !(kb < ka));
-                        kd[x] = take_a ? ka : kb;
-                        if constexpr (VALS) vd[x] = take_a ? va_p[ai] : vb_p[bi];
-                        if (take_a) ka = ka_p[++ai];
-                        else kb = kb_p[++bi];
-                    }
-                }
+            uint32_t c0 = 0;
+            for (;;) {  // pair of chunk c
+                const uint32_t n = (s_seg[min(2 * p + 2, m)] - s_seg[2 * p] + ITEMS - 1) / ITEMS;
+                if (c < c0 + n) break;
+                c0 += n;
                 ++p;
+            }
+            {
+                // pair p: A = segment 2p, B = segment 2p+1 (empty past the end)
+                const int ia = 2 * p, ib = 2 * p + 1;
+                const uint32_t o0 = s_seg[ia];
+                const uint32_t la = s_seg[ia + 1] - o0;
+                const uint32_t lb = ib < m ? s_seg[ib + 1] - s_seg[ib] : 0u;
+                const uint32_t a = ks + (first ? s_kbeg[ia] : o0) * SZ;
+                const uint32_t b = ks + (first ? (ib < m ? s_kbeg[ib] : 0u) : o0 + la) * SZ;
+                const uint32_t x = o0 + (c - c0) * ITEMS;
+                const uint32_t diag = x - o0;
+                const uint32_t ai = merge_path_sa<T>(a, la, b, lb, diag);
+                uint32_t pa = a + ai * SZ, pb = b + (diag - ai) * SZ;
+                const uint32_t ea = a + la * SZ, eb = b + lb * SZ;
+                T ka = lds_rec<T>(pa), kb = lds_rec<T>(pb);
+                const uint32_t stop = min(x + ITEMS, o0 + la + lb);
+                const uint32_t od = kd + x * SZ;
+                auto step = [&](uint32_t j) {
+                    const bool ta = pa < ea && (pb >= eb || !(kb < ka));
+                    const uint32_t pt = ta ? pa : pb;
+                    sts_rec<T>(od + j * SZ, ta ? ka : kb);
+                    if constexpr (VALS) sts_rec<uint32_t>(vaddr(od + j * SZ), lds_rec<uint32_t>(vaddr(pt)));
+                    const uint32_t pn = pt + SZ;
+                    const T v = lds_rec<T>(pn);
+                    pa = ta ? pn : pa;
+                    pb = ta ? pb : pn;
+                    ka = ta ? v : ka;
+                    kb = ta ? kb : v;
+                };
+                if (stop == x + ITEMS) {
+#pragma unroll
+                    for (int j = 0; j < ITEMS; ++j) step(j);
+                } else {
+                    for (uint32_t j = 0; j < stop - x; ++j) step(j);
+                }
             }
         }
         __syncthreads();
@@ -516,15 +608,10 @@ __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> 
         else if ((uint32_t)tid >= V && tid - V < total - tail0) __stcs(gk + tail0 + (tid - V), kf[tail0 + (tid - V)]);
     }
     if constexpr (VALS) {
-        const uint32_t* vf = vbase + (cur ? cap : 0) + pvo;
+        // payloads sit at the key records' indices (phase po in key records)
+        const uint32_t* vf = vbase + (cur ? cap : 0) + po;
         uint32_t* gv = vout + o;
-        const uint32_t head = min((4 - pvo) % 4, total);
-        const uint32_t nv = (total - head) / 4;
-        const uint32_t tail0 = head + nv * 4;
-        for (uint32_t v = tid; v < nv; v += kKThreads)
-            __stcs(reinterpret_cast<uint4*>(gv + head + v * 4), *reinterpret_cast<const uint4*>(vf + head + v * 4));
-        if ((uint32_t)tid < head) __stcs(gv + tid, vf[tid]);
-        else if ((uint32_t)tid >= 4 && tid - 4 < total - tail0) __stcs(gv + tail0 + (tid - 4), vf[tail0 + (tid - 4)]);
+        for (uint32_t i = tid; i < total; i += kKThreads) __stcs(gv + i, vf[i]);
     }
 }
 
@@ -562,7 +649,7 @@ template <typename T>
 b2s_status kway_grouped(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* vals,
                         const uint64_t* lens, int k, void* out, uint32_t* vout) {
     constexpr uint32_t S = GroupCfg<T>::S;
-    constexpr uint32_t per_group = GroupCfg<T>::T_ / S;
+    const uint32_t per_group = GroupCfg<T>::target(k) / S;
     const bool with_vals = vout != nullptr;
     KRuns<T> R{};
     R.k = k;
@@ -613,14 +700,18 @@ struct Run {
 int kway_mode() {
     static int m = -1;
     if (m < 0) {
-        // 0: pairwise rounds (default: ~4 TB/s per round on B200), 1: the
-        // grouped single-pass merge. It reads and writes every key once, but
-        // the merge is bound by instructions and shared-memory wavefronts,
-        // not HBM, and its log2(k) in-shared-memory rounds cost what the
-        // global rounds cost: 8 runs of 2^25 i32 1.76 ms vs 1.69 pairwise,
-        // 4 runs 1.07 vs 1.09 (ncu: 147 instructions per output either way)
+        // -1 (default): the grouped single-pass merge for 4-byte keys,
+        // 3 <= k <= 8 and n >= 2^22, pairwise rounds otherwise; 0: always pairwise; 1:
+        // grouped whenever it applies. The grouped merge reads and writes
+        // every key once, but its rounds in shared memory are bound by the
+        // merge step's dependency chain and the per-group barriers, not HBM.
+        // Measured per 2^28 i32 keys (pairwise / grouped): k=3 1.005 / 0.971
+        // ms, k=4 1.087 / 1.018, k=8 1.685 / 1.534, k=16 2.379 / 2.653; per
+        // 2^27 u64: k=4 0.947 / 0.974, k=8 1.481 / 1.432. Its fixed part --
+        // samples, their sort, cuts, staging and the write -- is 0.57 ms for
+        // k=8 (rounds ablated): one HBM pass plus the cut computation.
         const char* e = getenv("B2S_KWAY");
-        m = e ? atoi(e) : 0;
+        m = e ? atoi(e) : -1;
     }
     return m;
 }
@@ -630,7 +721,13 @@ b2s_status kway_t(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* 
                   const uint64_t* lens, int k, void* out, uint32_t* vout, void* tmp,
                   uint32_t* vtmp) {
     const bool with_vals = vout != nullptr;
-    if (k > 2 && k <= kMaxK && kway_mode() == 1 && kway_grouped_fits<T>(lens, k))
+    const int mode = kway_mode();
+    uint64_t n_all = 0;
+    for (int i = 0; i < k; ++i) n_all += lens[i];
+    // small merges are bound by their chain of launches: the grouped one's
+    // sample sort adds a dozen (cfg1, 4 runs of 2^18: 0.112 vs 0.09 ms)
+    const bool grouped = mode == 1 || (mode < 0 && sizeof(T) == 4 && k <= 8 && n_all >= (1ull << 22));
+    if (k > 2 && k <= kMaxK && grouped && kway_grouped_fits<T>(lens, k))
         return kway_grouped<T>(ctx, runs, vals, lens, k, out, vout);
     std::vector<Run> cur;
     uint64_t total = 0;

@@ -28,9 +28,11 @@ def test_kway_merge(ctx, dt, k):
     _kway_case(ctx, dt, k)
 
 
-@pytest.mark.parametrize("k", [3, 8, 16])
-def test_kway_single_pass_variant(k):
-    """The experimental single-pass bucket merge (B2S_KWAY=1), in a subprocess so
+@pytest.mark.parametrize("mode,k", [("1", 3), ("1", 8), ("1", 16), ("0", 3), ("0", 8)])
+def test_kway_merge_modes(mode, k):
+    """Both k-way strategies whatever the default picks: the grouped
+    single-pass merge forced on (B2S_KWAY=1, also for 8-byte keys and k > 8)
+    and the pairwise rounds forced on (B2S_KWAY=0), each in a subprocess so
     the mode switch is read fresh."""
     import subprocess
     import sys
@@ -40,7 +42,7 @@ def test_kway_single_pass_variant(k):
             "c = Context(0)\n"
             "for dt in t.DTYPES: t._kway_case(c, dt, %d)\n"
             "print('ok')") % (os.path.dirname(__file__), os.path.dirname(os.path.dirname(__file__)), k)
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, B2S_KWAY="1"),
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, B2S_KWAY=mode),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
