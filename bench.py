@@ -541,7 +541,12 @@ def run_multi(args, rank: int, world: int):
                          "kernel": "onesweep_kernel (one digit pass, rank 0)",
                          "peak_kind": peak_kind,
                          "combined_hbm_nvlink_frac": t_roof_ms / ms_step,
-                         "combined_roofline_ms": t_roof_ms},
+                         "combined_roofline_ms": t_roof_ms,
+                         "hbm_bytes_per_gpu": hbm_bytes,
+                         "nvlink_bytes_per_gpu": nvl_bytes,
+                         "nvlink_peak_gbs": nvlink_gbs,
+                         "nvlink_peak_kind": "B200_PROFILING.md peer-copy figure (not measurable "
+                                             "on the one-GPU development box)"},
             "phases_ms": phases, "bucket_sizes": buckets,
             "e2e": {"value": total / float(e2e_s.item()), "unit": UNIT,
                     "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": d2h,

@@ -95,6 +95,7 @@ class SampleSorter:
         self.last_phase_ms = {}
         self.last_bucket_sizes = []
         self._timing = ctx is not None and ops is None
+        self._hinfo = None  # p2p: (handle, payload offset) and its device copy
 
     @property
     def rank(self) -> int:
@@ -206,15 +207,22 @@ class SampleSorter:
         bounds = self.ops.bounds(skeys, rank, splitters, world)
         ev.mark("splitters")
 
-        # every rank's bounds, buffer handle and payload offset: world x (G+1+8+1)
-        hdl = torch.frombuffer(bytearray(handle), dtype=torch.int64)
-        info = torch.cat([bounds.to(torch.int64).cpu(), hdl, torch.tensor([voff])])
+        # every rank's bounds, buffer handle and payload offset: world x (G+1+8+1),
+        # gathered on the device; the host reads the result once per step (the
+        # merge takes host pointers and lengths). The handle part is uploaded
+        # only when this rank's buffer or payload offset changed.
+        hkey = (handle, voff)
+        if self._hinfo is None or self._hinfo[0] != hkey:
+            hdl = torch.frombuffer(bytearray(handle), dtype=torch.int64)
+            self._hinfo = (hkey, torch.cat([hdl, torch.tensor([voff])]).to(keys.device))
         if gloo:
+            info = torch.cat([bounds.to(torch.int64).cpu(), self._hinfo[1].cpu()])
             allinfo = torch.empty(world * info.numel(), dtype=torch.int64)
             dist.all_gather_into_tensor(allinfo, info, group=self.group)
         else:
+            info = torch.cat([bounds.to(torch.int64), self._hinfo[1]])
             allinfo = torch.empty(world * info.numel(), dtype=torch.int64, device=keys.device)
-            dist.all_gather_into_tensor(allinfo, info.to(keys.device), group=self.group)
+            dist.all_gather_into_tensor(allinfo, info, group=self.group)
             allinfo = allinfo.cpu()
         allinfo = allinfo.view(world, -1)
         rows = allinfo.tolist()
