@@ -642,8 +642,10 @@ struct NextDigit {
 // Shared state of one CTA besides the tile buffers.
 template <typename LB>
 struct TileShared {
-    using OFF = LB;  // 32-bit offsets exactly when the look-back words are 32-bit (n < 2^30)
+    using OFF = LB;  // 32-bit offsets exactly when the look-back words are 32-bit (n <= 2^31)
     OFF goff[kRadix];    // the slot's global digit offsets
+    uint32_t dcount[sizeof(LB) == 4 ? kRadix : 1];  // 32-bit words: the slot's digit totals
+    unsigned long long n;
     uint32_t nhist[kRadix];
     uint32_t start[kRadix];
     uint32_t wsum[kRadix / 32];
@@ -659,14 +661,19 @@ struct TileShared {
 // predecessors were fetched into `lbw` by cp.async before the ranking; later
 // steps read B2S_LB_STEP at a time (independent loads) in a warp-uniform loop.
 // The tile's inclusive prefix is published the moment it is known.
+// 32-bit words hold prefixes modulo 2^30; `lo` is a lower bound of the true
+// exclusive prefix less than 2^30 below it (see exclusive_floor), which makes
+// the residue exact.
 template <typename LB>
 __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, LB* __restrict__ lb_cur,
-                                                                 const LB* lbw, uint32_t mycount) {
+                                                                 const LB* lbw, uint32_t mycount,
+                                                                 unsigned long long lo) {
     using W = LookbackWord<LB>;
     constexpr int PRE = W::kPrefetch;
     constexpr int LOOKBACK = B2S_LB_STEP;
     const int tid = threadIdx.x;
     unsigned long long excl = 0;
+    (void)lo;
     if (tile == 0) return 0;
     int64_t pred = (int64_t)tile - 1;
     bool done = false;
@@ -689,7 +696,7 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, 
             }
         }
     }
-    if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
+    if (done) st_relaxed(mine, W::kInc | ((LB)(excl + mycount) & W::kMask));
     while (__any_sync(0xffffffffu, !done)) {
         if (!done) {
             LB w[LOOKBACK];
@@ -709,9 +716,10 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, 
                     stop = true;
                 }
             }
-            if (done) st_relaxed(mine, W::kInc | (LB)(excl + mycount));
+            if (done) st_relaxed(mine, W::kInc | ((LB)(excl + mycount) & W::kMask));
         }
     }
+    if constexpr (sizeof(LB) == 4) excl = lo + ((excl - lo) & W::kMask);
     return excl;
 }
 
@@ -1035,7 +1043,16 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     auto lookback = [&]() {
         if (tid < kRadix) {
             const uint32_t mycount = (tid + 1 < kRadix ? sh.start[tid + 1] : (uint32_t)tile_valid) - sh.start[tid];
-            const unsigned long long excl = lookback_exclusive<LB>(tile, lb_cur, sh.lbw, mycount);
+            // 32-bit words: digit tid's keys in tiles >= tile number at most
+            // the keys from tile_base on, so its exclusive prefix is at
+            // least dcount - (n - tile_base); the prefix is at most
+            // min(tile_base, dcount), a window narrower than 2^30 (below)
+            unsigned long long lo = 0;
+            if constexpr (sizeof(LB) == 4) {
+                const unsigned long long rest = sh.n - tile_base;
+                lo = sh.dcount[tid] > rest ? sh.dcount[tid] - rest : 0;
+            }
+            const unsigned long long excl = lookback_exclusive<LB>(tile, lb_cur, sh.lbw, mycount, lo);
             gbase_out[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
         }
     };
@@ -1329,6 +1346,8 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         }
         if (lane == 31) sh.wsum64[tid >> 5] = incl;
         sh.goff[tid] = (typename TileShared<LB>::OFF)(incl - c);
+        if constexpr (sizeof(LB) == 4) sh.dcount[tid] = (uint32_t)c;
+        if (tid == 0) sh.n = n;
         sh.nhist[tid] = 0;
     }
     for (int i = tid; i < SM::WARPS * (kRadix / 2); i += THREADS) s_cnt[i] = 0;
@@ -1575,6 +1594,23 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
     }
 }
 
+uint64_t lookback_tile(uint64_t n, int kbytes, bool vals) {
+    const TileCfg c = tile_cfg(kbytes, vals, n);
+    return (uint64_t)c.threads * c.items;
+}
+
+// 32-bit look-back words (2 flag bits, prefixes modulo 2^30) are exact when
+// the window a tile's exclusive prefix can lie in is narrower than 2^30. For
+// tile k of T keys and a digit of H keys the prefix E satisfies
+//   max(0, H - (n - kT)) <= E <= min(kT, H),
+// a window of at most min(kT, n - kT) <= n / 2 keys, equal to n / 2 only when
+// kT = n / 2. So n <= 2^31 suffices, except n = 2^31 with T dividing 2^30.
+// (64-bit words cost cfg3 -- 2^31 i32 -- 3.6% per pass.)
+bool narrow_lookback_words(uint64_t n, uint64_t tile) {
+    const uint64_t half = 1ull << 30;
+    return n < 2 * half || (n == 2 * half && half % tile != 0);
+}
+
 template <typename U, bool VALS>
 b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kout,
                         const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc) {
@@ -1594,7 +1630,7 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
     }
     RadixPlan* plan = sc->plan;
     RadixCounters* ctr = sc->ctr;
-    const bool wide = n >= (1ull << 30);
+    const bool wide = !narrow_lookback_words(n, lookback_tile(n, (int)sizeof(U), VALS));
     ctx->ev_hist0 = record(ctx);
     B2S_CUDA(cudaMemsetAsync(ctr, 0, sizeof(RadixCounters), ctx->stream));
     // 4-byte keys past a few million: every digit histogram up front. 8-byte
@@ -1709,10 +1745,9 @@ extern "C" int b2s_debug_phase_cycles(unsigned long long* out16, int reset) {
 #endif
 
 size_t lookback_region_bytes(uint64_t n, int kbytes, bool vals) {
-    const TileCfg c = tile_cfg(kbytes, vals, n);
-    const uint64_t tile = (uint64_t)c.threads * c.items;
+    const uint64_t tile = lookback_tile(n, kbytes, vals);
     const uint64_t ntiles = (n + tile - 1) / tile;
-    return ntiles * kRadix * (n >= (1ull << 30) ? 8 : 4);
+    return ntiles * kRadix * (narrow_lookback_words(n, tile) ? 4 : 8);
 }
 
 b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout,

@@ -86,3 +86,23 @@ def test_cfg5_full(ctx):
     _check(ctx, "cfg5", keys, ok)
     _, vfp, _ = ctx.check_sorted(ov)
     assert vfp == int(GOLD["cfg5"]["payload_fp"]), "cfg5: payload order differs from the stable order"
+
+
+@pytest.mark.parametrize("n", [3 << 29, 1 << 31])
+def test_narrow_lookback_words_past_2_30(ctx, n):
+    """Between 2^30 and 2^31 keys the look-back words stay 32-bit and hold
+    prefixes modulo 2^30 (radix_sort.cu narrow_lookback_words). A digit with
+    more than 2^30 keys makes its prefixes wrap: 3 keys in 4 get low byte 7
+    (the skewed pass), so the first pass resolves prefixes past 2^30."""
+    keys = ctx.gen_keys(n, 5, torch.int32, shift=32)
+    hot = ((keys >> 8) & 3) != 0
+    keys = torch.where(hot, (keys & ~0xFF) | 7, keys)
+    del hot
+    _, _, ms_in = ctx.check_sorted(keys)
+    out = torch.empty_like(keys)
+    ctx.sort(keys, out=out)
+    inv, _, ms = ctx.check_sorted(out)
+    assert inv == 0, f"{inv} adjacent inversions"
+    assert ms == ms_in, "output is not a permutation of the input"
+    del keys, out
+    torch.cuda.empty_cache()
