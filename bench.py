@@ -350,7 +350,9 @@ def run_single(args):
     torch.cuda.empty_cache()
     hin_np = h_in.numpy()
     hout_np = h_out.numpy()
-    e2e_steps = max(3, min(args.steps, 6))
+    # one batch per timed step (the stream's fill and drain amortise over the
+    # run, as in a serving loop), at most 24 (~5 s of PCIe)
+    e2e_steps = max(3, min(args.steps, 24))
     ctx.sort_batch([hin_np] * 3, outs=[hout_np] * 3)  # warm the three staging buffers
     t0 = time.perf_counter()
     ctx.sort_batch([hin_np] * e2e_steps, outs=[hout_np] * e2e_steps)
@@ -484,7 +486,7 @@ def run_multi(args, rank: int, world: int):
     dbuf = [torch.empty_like(keys), torch.empty_like(keys)]
     ev_up = [torch.cuda.Event(), torch.cuda.Event()]
     ev_used = [None, None]  # the sort that read dbuf[b] last
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(2, min(args.steps, 24))
     dist.barrier()
     t0 = time.perf_counter()
     d2h = 0
