@@ -298,7 +298,10 @@ b2s_status merge2_window(b2s_ctx* ctx, const T* a, const uint32_t* va, uint64_t 
 //    (the sum of its lower cuts) with coalesced stores.
 
 constexpr int kMaxK = 16;
-constexpr int kKThreads = 256;
+#ifndef B2S_KG_THREADS
+#define B2S_KG_THREADS 256
+#endif
+constexpr int kKThreads = B2S_KG_THREADS;
 
 #ifndef B2S_KG_CAP
 #define B2S_KG_CAP 8192  // records per group (4-byte keys): 256 threads x 33 items, two CTAs per SM
