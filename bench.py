@@ -175,14 +175,15 @@ def ref_sample_size(budget_s: float, cap: int = N_TOTAL) -> tuple[int, str]:
     return n, why
 
 
-def cpu_reference(sample_n: int, reps: int = 3, shift: int = 33):
+def cpu_reference(sample_n: int, reps: int = 3, shift: int = 33, data=None):
     """parallel::scatter_merge_sort (merge, wall mode, p = k = host threads) on
     `sample_n` keys of the workload's distribution widened to int64;
     run_benchmark's semantics: median of reps of the world's wall seconds
     (P/src/bench.cpp:106-169)."""
     import oracle
     threads = max(1, min(os.cpu_count() or 1, 64))
-    data = _ref_keys(sample_n, shift)
+    if data is None:
+        data = _ref_keys(sample_n, shift)
     if oracle.ref_available():
         kind = "reference"
         times = []
@@ -213,8 +214,9 @@ def run_reference_arm(args, rank: int, world: int):
         ref_sample_size(per_step)
     vals = []
     base = None
+    data = _ref_keys(sample_n)  # generated once; each step sorts a fresh copy inside the reference
     for i in range(args.warmup + args.steps):
-        b = cpu_reference(sample_n, reps=1)
+        b = cpu_reference(sample_n, reps=1, data=data)
         if i >= args.warmup:
             vals.append(b["value"])
         base = b
