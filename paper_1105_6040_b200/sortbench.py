@@ -264,8 +264,10 @@ def gen_data(n: int, seed: int, device: bool = False):
 
 def verify_output(input_data, output) -> None:
     """bench::verify_output (P/src/bench.cpp:95-104): raises VerificationError
-    unless output is sorted and a permutation of input. Both checks run on the
-    GPU (inversion count + multiset hash, then an exact sorted comparison)."""
+    unless output is sorted and a permutation of input. The checks run on the
+    GPU: inversion count + multiset hash (b2s_check_sorted), then exact
+    equality with an independent sort of the input (torch.sort, CUB's), the
+    reference's std::sort(copy(input)) comparison."""
     import torch
 
     def dev(x):
@@ -279,6 +281,17 @@ def verify_output(input_data, output) -> None:
     _, _, ms_in = ctx.check_sorted(a)
     if inv != 0 or ms_in != ms_out:
         raise VerificationError("run produced output that is not the sorted input")
-    ref, _ = ctx.sort(a)
-    if not torch.equal(ref, b):
+    if not torch.equal(_independent_sort(a), b):
         raise VerificationError("run produced output that is not the sorted input")
+
+
+def _independent_sort(a):
+    """The ascending order of a device tensor by torch.sort (not this
+    library): unsigned keys are sorted through an order-preserving signed view."""
+    import torch
+    if a.dtype in (torch.uint32, torch.uint64):
+        signed = torch.int32 if a.dtype == torch.uint32 else torch.int64
+        flip = torch.tensor(-(1 << (8 * a.element_size() - 1)), dtype=signed, device=a.device)
+        s = torch.sort(a.view(signed) ^ flip)[0] ^ flip
+        return s.view(a.dtype)
+    return torch.sort(a)[0]

@@ -183,3 +183,22 @@ def test_gpu_run_benchmark_report_and_trace(tmp_path):
     assert all(json.loads(l)["run_id"] == R.run_id(reps[2].config) for l in lines)
     summ = json.load(open(path + ".summary.json"))
     assert summ["procs"] == 4 and len(summ["ranks"]) == 4
+
+
+@pytest.mark.parametrize("dt", ["uint32", "uint64", "int32"])
+def test_verify_output_device_keys(dt):
+    """verify_output on device tensors of every key type: the exact check is
+    an independent sort (torch.sort through an order-preserving signed view
+    for unsigned keys), so a high-bit key must land last."""
+    import torch
+    tdt = getattr(torch, dt)
+    npdt = np.dtype(dt)
+    hi = (1 << (8 * npdt.itemsize - 1)) + 5 if dt.startswith("u") else -7
+    host = np.array([3, 1, hi, 2], dtype=npdt)
+    signed = np.dtype(f"int{8 * npdt.itemsize}")
+    inp = torch.from_numpy(host.view(signed)).cuda().view(tdt)
+    good = sb._independent_sort(inp)
+    sb.verify_output(inp, good)
+    bad = good.flip(0)
+    with pytest.raises(sb.VerificationError):
+        sb.verify_output(inp, bad)
