@@ -117,6 +117,7 @@ struct RadixCounters {
     unsigned long long or_all;                // OR of all keys
     unsigned long long nor_all;               // OR of all complemented keys
     unsigned long long asc_pairs, desc_pairs;  // sampled adjacent pairs in order / reversed
+    unsigned long long ticket[256];            // keys-only first pass: digit offsets in tile arrival order
 };
 
 struct TimingEvents {

@@ -463,6 +463,9 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_LB_STEP
 #define B2S_LB_STEP 4
 #endif
+#ifndef B2S_TICKET_FIRST
+#define B2S_TICKET_FIRST 1  // keys-only first pass: offsets by fetch-and-add, no look-back
+#endif
 #ifndef B2S_TMA_EVICT_FIRST
 #define B2S_TMA_EVICT_FIRST 1
 #endif
@@ -844,7 +847,8 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                                               const U* __restrict__ src, U* __restrict__ dst,
                                               const uint32_t* __restrict__ vsrc,
                                               uint32_t* __restrict__ vdst, LB* __restrict__ lb_cur,
-                                              int shift, uint32_t dxor, const NextDigit nd,
+                                              unsigned long long* __restrict__ ticket, int shift,
+                                              uint32_t dxor, const NextDigit nd,
                                               uint32_t* s_cnt, U* kbuf, uint32_t* vbuf,
                                               U* sbuf, uint32_t* svbuf,
                                               uint32_t* s_match, uint32_t* s_early,
@@ -987,10 +991,12 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             pair += c;
         }
         const uint32_t c0 = pair & 0xFFFFu, c1 = pair >> 16;
-        LB* slot = lb_cur + (size_t)tile * kRadix + 2 * tid;
-        const LB flag = tile == 0 ? W::kInc : W::kAgg;
-        st_relaxed(slot, flag | (LB)c0);
-        st_relaxed(slot + 1, flag | (LB)c1);
+        if (ticket == nullptr) {
+            LB* slot = lb_cur + (size_t)tile * kRadix + 2 * tid;
+            const LB flag = tile == 0 ? W::kInc : W::kAgg;
+            st_relaxed(slot, flag | (LB)c0);
+            st_relaxed(slot + 1, flag | (LB)c1);
+        }
         uint32_t incl = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1005,7 +1011,7 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // registers held) so their latency hides behind the ranking below. A stale
     // copy is harmless: a slot only moves 0 -> aggregate -> inclusive and every
     // non-zero state is valid; zeros are re-polled.
-    if (tid < kRadix && tile > 0) {
+    if (tid < kRadix && tile > 0 && ticket == nullptr) {
 #pragma unroll
         for (int i = 0; i < PRE; ++i) {
             if ((int64_t)tile - 1 - i >= 0)
@@ -1052,7 +1058,11 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
                 const unsigned long long rest = sh.n - tile_base;
                 lo = sh.dcount[tid] > rest ? sh.dcount[tid] - rest : 0;
             }
-            const unsigned long long excl = lookback_exclusive<LB>(tile, lb_cur, sh.lbw, mycount, lo);
+            // keys-only first pass: no order to keep among equal digits, so
+            // a tile's offsets come from one fetch-and-add per digit in
+            // arrival order -- no look-back chain
+            const unsigned long long excl = ticket != nullptr ? atomicAdd(ticket + tid, (unsigned long long)mycount)
+                                                              : lookback_exclusive<LB>(tile, lb_cur, sh.lbw, mycount, lo);
             gbase_out[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
         }
     };
@@ -1310,6 +1320,9 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
 
     const int shift = 8 * plan->digit[slot];
     const uint32_t dxor = plan->dxor[slot];
+    // a keys-only sort's first pass need not be stable: equal keys are
+    // indistinguishable and no earlier pass's order is to be kept
+    unsigned long long* const ticket = (!VALS && slot == 0 && B2S_TICKET_FIRST) ? ctr->ticket : nullptr;
     const U* src = static_cast<const U*>(plan->ksrc[slot]);
     U* dst = static_cast<U*>(plan->kdst[slot]);
     const uint32_t* vsrc = plan->vsrc[slot];
@@ -1404,16 +1417,19 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
                 parity ^= 1u << lb_;
                 B2S_PHASE(0);
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, true, TR, SWZ, SEP>(
-                    claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
+                    claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, ticket, shift,
+                    dxor, nd, s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t,
+                    hot);
             } else {
                 onesweep_tile<U, VALS, LB, THREADS, ITEMS, true, false, TR, SWZ, SEP>(
-                    claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor, nd,
-                    s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
+                    claim, publish, s_gbase, tile, TILE, tile_base, src, dst, vsrc, vdst, lb_cur, ticket, shift,
+                    dxor, nd, s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t,
+                    hot);
             }
         } else {
             onesweep_tile<U, VALS, LB, THREADS, ITEMS, false, false, TR, SWZ, SEP>(
-                claim, publish, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, shift, dxor,
+                claim, publish, s_gbase, tile, (uint32_t)rem, tile_base, src, dst, vsrc, vdst, lb_cur, ticket,
+                shift, dxor,
                 nd, s_cnt, kbuf[lb_], vbuf[lb_], kbuf[sb_], vbuf[sb_], idle, idle, sh, prof_acc, prof_t, hot);
         }
         // Between two full TMA tiles of the early-rank kernels no barrier is
