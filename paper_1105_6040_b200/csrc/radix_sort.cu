@@ -1663,9 +1663,11 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
         }));
         const uint64_t want = (n / (16 / sizeof(U)) + kAllHistThreads * 4 - 1) / (kAllHistThreads * 4);
         const int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)ctx->num_sms);
+        // look-back region 0 serves the first pass, which a keys-only sort
+        // runs without look-back (tickets): nothing to zero then
+        const size_t zero16 = (!VALS && B2S_TICKET_FIRST) ? 0 : (lb_region + 15) / 16;
         radix_prologue_all_kernel<U><<<grid, kAllHistThreads, kAllHistSmem, ctx->stream>>>(
-            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
-            (lb_region + 15) / 16, top_xor);
+            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback), zero16, top_xor);
         B2S_LAUNCHED();
     } else {
         const int threads = 512;
