@@ -90,6 +90,11 @@ int b2s_device_count(void);
 /* Kernels this library has launched in this process (all contexts); the
  * difference across a region counts the region's launches. */
 unsigned long long b2s_kernel_launches(void);
+/* 1 when the context ranks keys with lane-ordered shared atomics (the probe
+ * at b2s_create found same-word lanes of one atomic served in lane order on
+ * this device), 0 when it fell back to ballot matching (also B2S_RANK=ballot);
+ * -1 for a bad context. Both are stable; the atomic ranking is the fast one. */
+int b2s_lane_ordered_atomics(b2s_ctx* ctx);
 
 /* ---- multi-GPU pull exchange (one process per GPU) ------------------------
  * Replaces the reference's rank-to-rank block messages (Comm::send/recv and

@@ -20,7 +20,7 @@ B2S_DEVICE, B2S_HOST = 0, 1
 # every symbol include/b200sort.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "b2s_create", "b2s_destroy", "b2s_set_stream", "b2s_synchronize", "b2s_enable_timing",
-    "b2s_get_timing", "b2s_last_error", "b2s_version", "b2s_device_count", "b2s_kernel_launches", "b2s_sort",
+    "b2s_get_timing", "b2s_last_error", "b2s_version", "b2s_device_count", "b2s_kernel_launches", "b2s_lane_ordered_atomics", "b2s_sort",
     "b2s_merge", "b2s_sort_batch", "b2s_partitioned_sort", "b2s_odd_even_sort", "b2s_plan_partition",
     "b2s_merge_split_padded",
     "b2s_sample_regular", "b2s_select_splitters", "b2s_bucket_bounds", "b2s_gen_keys",
@@ -76,6 +76,7 @@ _SIGS = {
     "b2s_version": (ctypes.c_char_p, []),
     "b2s_device_count": (_i, []),
     "b2s_kernel_launches": (ctypes.c_ulonglong, []),
+    "b2s_lane_ordered_atomics": (_i, [_p]),
     "b2s_sort": (_st, [_p, _i, _p, _p, _p, _p, _u64, _u32]),
     "b2s_merge": (_st, [_p, _i, _p, _p, _p, _i, _p, _p, _u32]),
     "b2s_sort_batch": (_st, [_p, _i, _p, _p, _p, _p, _u64, _i, _u32]),

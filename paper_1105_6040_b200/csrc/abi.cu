@@ -155,6 +155,11 @@ const char* b2s_version(void) { return "b200sort 0.1 (sm_100a onesweep radix + m
 
 unsigned long long b2s_kernel_launches(void) { return b2s::launch_count(); }
 
+int b2s_lane_ordered_atomics(b2s_ctx* ctx) {
+    if (check_ctx(ctx) != B2S_OK) return -1;
+    return ctx->atomic_rank ? 1 : 0;
+}
+
 b2s_status b2s_exchange_buffer(b2s_ctx* ctx, uint64_t bytes, void** ptr, void* handle64) {
     B2S_TRY(check_ctx(ctx));
     if (ptr == nullptr || handle64 == nullptr) return set_error(B2S_EINVAL, "null output");

@@ -1709,11 +1709,14 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
 
 // Checks the property the atomic ranking relies on: lanes of one warp
 // instruction adding to the same shared counter get old values in ascending
-// lane order. Every warp keeps private counters; digit patterns run from one
-// bin (all lanes collide) to 256 bins.
+// lane order -- with the packed 16-bit counters and the inline-PTX atomics
+// the ranking issues, also when some lanes are predicated off (the skewed
+// pass's hot-digit lanes). Every warp keeps private counters; digit patterns
+// run from one bin (all lanes collide) to 256 bins.
 __global__ void probe_lane_order_kernel(int iters, unsigned long long* bad) {
     __shared__ uint32_t cnt[8][kRadix / 2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
     uint32_t x = 0x9E3779B9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
     unsigned long long nb = 0;
     for (int it = 0; it < iters; ++it) {
@@ -1725,9 +1728,12 @@ __global__ void probe_lane_order_kernel(int iters, unsigned long long* bad) {
         const uint32_t bins = 1u << (it % 9);
         const uint32_t d = (x >> 8) % bins;
         const uint32_t sh16 = 16 * (d & 1);
-        const uint32_t r = (atomicAdd(&cnt[warp][d >> 1], 1u << sh16) >> sh16) & 0xFFFFu;
-        const uint32_t peers = match_digit<8>(d);
-        nb += (r != (uint32_t)__popc(peers & ((1u << lane) - 1u)));
+        // odd iterations: about one lane in four sits out
+        const bool on = (it & 1) == 0 || (x & 3) != 0;
+        const uint32_t a = smem_addr(&cnt[warp][d >> 1]);
+        const uint32_t r = (atom_add_shared_if(on, a, 1u << sh16) >> sh16) & 0xFFFFu;
+        const uint32_t peers = match_digit<8>(d) & __ballot_sync(0xffffffffu, on);
+        nb += on && (r != (uint32_t)__popc(peers & lt));
         __syncwarp();
     }
     if (nb) atomicAdd(bad, nb);

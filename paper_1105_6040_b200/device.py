@@ -118,6 +118,12 @@ class Context:
     def synchronize(self) -> None:
         check(lib().b2s_synchronize(self._h))
 
+    @property
+    def lane_ordered_atomics(self) -> bool:
+        """True when keys are ranked by lane-ordered shared atomics (the probe
+        at context creation passed), False on the ballot-matching fallback."""
+        return lib().b2s_lane_ordered_atomics(self._h) == 1
+
     def enable_timing(self, on: bool = True) -> None:
         check(lib().b2s_enable_timing(self._h, int(on)))
 

@@ -312,3 +312,11 @@ def test_all_digit_prologue_pairs_and_unaligned(ctx, dt):
     out, _ = ctx.sort(d)
     torch.cuda.synchronize()
     assert np.array_equal(to_host(out, dt), np.sort(keys[1:]))
+
+
+def test_lane_ordered_atomics_probe(ctx):
+    """On B200 the probe at context creation finds same-word lanes of one
+    shared atomic served in lane order -- also with lanes predicated off --
+    so the fast ranking is the one in use (a silent fallback to ballot
+    matching would stay correct but slow)."""
+    assert ctx.lane_ordered_atomics
