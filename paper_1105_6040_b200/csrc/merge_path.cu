@@ -304,10 +304,10 @@ constexpr int kMaxK = 16;
 constexpr int kKThreads = B2S_KG_THREADS;
 
 #ifndef B2S_KG_CAP
-#define B2S_KG_CAP 8192  // records per group (4-byte keys): 256 threads x 33 items, two CTAs per SM
+#define B2S_KG_CAP 8192  // records per group (4-byte keys): two CTAs per SM
 #endif
 #ifndef B2S_KG_ITEMS
-#define B2S_KG_ITEMS 33
+#define B2S_KG_ITEMS 29
 #endif
 template <typename T>
 struct GroupCfg {
@@ -543,7 +543,14 @@ __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> 
         const int npairs = (m + 1) / 2;
         uint32_t nchunks = 0;
         for (int q = 0; q < npairs; ++q) nchunks += (s_seg[min(2 * q + 2, m)] - s_seg[2 * q] + ITEMS - 1) / ITEMS;
-        for (uint32_t c = tid; c < nchunks; c += kKThreads) {
+        // one merge chain per chunk: both heads and read positions as shared
+        // byte addresses; the per-output step is a compare, a store, one load
+        // of the taken side's next record and selects
+        struct Chain {
+            uint32_t pa, pb, ea, eb, od, n;
+            T ka, kb;
+        };
+        auto open = [&](uint32_t c, Chain& h) {
             int p = 0;
             uint32_t c0 = 0;
             for (;;) {  // pair of chunk c
@@ -552,40 +559,55 @@ __global__ void __launch_bounds__(kKThreads) kmerge_group_kernel(const KRuns<T> 
                 c0 += n;
                 ++p;
             }
-            {
-                // pair p: A = segment 2p, B = segment 2p+1 (empty past the end)
-                const int ia = 2 * p, ib = 2 * p + 1;
-                const uint32_t o0 = s_seg[ia];
-                const uint32_t la = s_seg[ia + 1] - o0;
-                const uint32_t lb = ib < m ? s_seg[ib + 1] - s_seg[ib] : 0u;
-                const uint32_t a = ks + (first ? s_kbeg[ia] : o0) * SZ;
-                const uint32_t b = ks + (first ? (ib < m ? s_kbeg[ib] : 0u) : o0 + la) * SZ;
-                const uint32_t x = o0 + (c - c0) * ITEMS;
-                const uint32_t diag = x - o0;
-                const uint32_t ai = merge_path_sa<T>(a, la, b, lb, diag);
-                uint32_t pa = a + ai * SZ, pb = b + (diag - ai) * SZ;
-                const uint32_t ea = a + la * SZ, eb = b + lb * SZ;
-                T ka = lds_rec<T>(pa), kb = lds_rec<T>(pb);
-                const uint32_t stop = min(x + ITEMS, o0 + la + lb);
-                const uint32_t od = kd + x * SZ;
-                auto step = [&](uint32_t j) {
-                    const bool ta = pa < ea && (pb >= eb || !(kb < ka));
-                    const uint32_t pt = ta ? pa : pb;
-                    sts_rec<T>(od + j * SZ, ta ? ka : kb);
-                    if constexpr (VALS) sts_rec<uint32_t>(vaddr(od + j * SZ), lds_rec<uint32_t>(vaddr(pt)));
-                    const uint32_t pn = pt + SZ;
-                    const T v = lds_rec<T>(pn);
-                    pa = ta ? pn : pa;
-                    pb = ta ? pb : pn;
-                    ka = ta ? v : ka;
-                    kb = ta ? kb : v;
-                };
-                if (stop == x + ITEMS) {
+            // pair p: A = segment 2p, B = segment 2p+1 (empty past the end)
+            const int ia = 2 * p, ib = 2 * p + 1;
+            const uint32_t o0 = s_seg[ia];
+            const uint32_t la = s_seg[ia + 1] - o0;
+            const uint32_t lb = ib < m ? s_seg[ib + 1] - s_seg[ib] : 0u;
+            const uint32_t a = ks + (first ? s_kbeg[ia] : o0) * SZ;
+            const uint32_t b = ks + (first ? (ib < m ? s_kbeg[ib] : 0u) : o0 + la) * SZ;
+            const uint32_t x = o0 + (c - c0) * ITEMS;
+            const uint32_t diag = x - o0;
+            const uint32_t ai = merge_path_sa<T>(a, la, b, lb, diag);
+            h.pa = a + ai * SZ;
+            h.pb = b + (diag - ai) * SZ;
+            h.ea = a + la * SZ;
+            h.eb = b + lb * SZ;
+            h.ka = lds_rec<T>(h.pa);
+            h.kb = lds_rec<T>(h.pb);
+            h.n = min((uint32_t)ITEMS, o0 + la + lb - x);
+            h.od = kd + x * SZ;
+        };
+        auto step = [&](Chain& h, uint32_t j) {
+            const bool ta = h.pa < h.ea && (h.pb >= h.eb || !(h.kb < h.ka));
+            const uint32_t pt = ta ? h.pa : h.pb;
+            sts_rec<T>(h.od + j * SZ, ta ? h.ka : h.kb);
+            if constexpr (VALS) sts_rec<uint32_t>(vaddr(h.od + j * SZ), lds_rec<uint32_t>(vaddr(pt)));
+            const uint32_t pn = pt + SZ;
+            const T v = lds_rec<T>(pn);
+            h.pa = ta ? pn : h.pa;
+            h.pb = ta ? h.pb : pn;
+            h.ka = ta ? v : h.ka;
+            h.kb = ta ? h.kb : v;
+        };
+        // two independent chains per thread (chunks c and c + kKThreads),
+        // stepped in lockstep so one's shared-load latency hides behind the
+        // other's compare and selects
+        for (uint32_t c = tid; c < nchunks; c += 2 * kKThreads) {
+            Chain h0, h1;
+            open(c, h0);
+            const bool two = c + kKThreads < nchunks;
+            if (two) open(c + kKThreads, h1);
+            if (two && h0.n == (uint32_t)ITEMS && h1.n == (uint32_t)ITEMS) {
 #pragma unroll
-                    for (int j = 0; j < ITEMS; ++j) step(j);
-                } else {
-                    for (uint32_t j = 0; j < stop - x; ++j) step(j);
+                for (int j = 0; j < ITEMS; ++j) {
+                    step(h0, j);
+                    step(h1, j);
                 }
+            } else {
+                for (uint32_t j = 0; j < h0.n; ++j) step(h0, j);
+                if (two)
+                    for (uint32_t j = 0; j < h1.n; ++j) step(h1, j);
             }
         }
         __syncthreads();
@@ -704,15 +726,14 @@ int kway_mode() {
     static int m = -1;
     if (m < 0) {
         // -1 (default): the grouped single-pass merge for 4-byte keys,
-        // 3 <= k <= 8 and n >= 2^22, pairwise rounds otherwise; 0: always pairwise; 1:
-        // grouped whenever it applies. The grouped merge reads and writes
-        // every key once, but its rounds in shared memory are bound by the
-        // merge step's dependency chain and the per-group barriers, not HBM.
-        // Measured per 2^28 i32 keys (pairwise / grouped): k=3 1.005 / 0.971
-        // ms, k=4 1.087 / 1.018, k=8 1.685 / 1.534, k=16 2.379 / 2.653; per
-        // 2^27 u64: k=4 0.947 / 0.974, k=8 1.481 / 1.432. Its fixed part --
-        // samples, their sort, cuts, staging and the write -- is 0.57 ms for
-        // k=8 (rounds ablated): one HBM pass plus the cut computation.
+        // 4 <= k <= 16 and n >= 2^22, pairwise rounds otherwise; 0: always
+        // pairwise; 1: grouped whenever it applies. The grouped merge reads
+        // and writes every key once, but its rounds in shared memory are
+        // bound by the merge step's dependency chain and the per-group
+        // barriers, not HBM. Measured per 2^28 i32 keys (pairwise / grouped):
+        // k=3 1.005 / 1.064 ms, k=4 1.087 / 0.963, k=8 1.685 / 1.388, k=16
+        // 2.379 / 2.317; per 2^27 u64: k=3 0.885 / 0.932, k=4 0.948 / 0.990,
+        // k=8 1.484 / 1.428, k=16 2.123 / 2.700.
         const char* e = getenv("B2S_KWAY");
         m = e ? atoi(e) : -1;
     }
@@ -729,7 +750,7 @@ b2s_status kway_t(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* 
     for (int i = 0; i < k; ++i) n_all += lens[i];
     // small merges are bound by their chain of launches: the grouped one's
     // sample sort adds a dozen (cfg1, 4 runs of 2^18: 0.112 vs 0.09 ms)
-    const bool grouped = mode == 1 || (mode < 0 && sizeof(T) == 4 && k <= 8 && n_all >= (1ull << 22));
+    const bool grouped = mode == 1 || (mode < 0 && sizeof(T) == 4 && k >= 4 && n_all >= (1ull << 22));
     if (k > 2 && k <= kMaxK && grouped && kway_grouped_fits<T>(lens, k))
         return kway_grouped<T>(ctx, runs, vals, lens, k, out, vout);
     std::vector<Run> cur;
