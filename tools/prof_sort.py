@@ -2,7 +2,7 @@
 
   python tools/prof_sort.py --n 67108864 --dtype u32 --iters 3 [--vals]
 Prints one line per iteration with the per-phase CUDA-event times.
-B2S_ONESWEEP_CFG selects the onesweep tile configuration.
+Tile configurations are build switches (B2S_U32_ITEMS; tools/kdev_build.sh).
 """
 import argparse
 import os
