@@ -106,3 +106,19 @@ def test_narrow_lookback_words_past_2_30(ctx, n):
     assert ms == ms_in, "output is not a permutation of the input"
     del keys, out
     torch.cuda.empty_cache()
+
+
+def test_wide_lookback_words_past_2_31(ctx):
+    """Above 2^31 keys the look-back words are 64-bit (the only sizes that
+    still use them): a sort of 2^31 + 3 * 2^20 + 7 int32 keys, with a
+    partial last tile, checked by order and multiset."""
+    n = (1 << 31) + 3 * (1 << 20) + 7
+    keys = ctx.gen_keys(n, 9, torch.int32, shift=32)
+    _, _, ms_in = ctx.check_sorted(keys)
+    out = torch.empty_like(keys)
+    ctx.sort(keys, out=out)
+    inv, _, ms = ctx.check_sorted(out)
+    assert inv == 0, f"{inv} adjacent inversions"
+    assert ms == ms_in, "output is not a permutation of the input"
+    del keys, out
+    torch.cuda.empty_cache()
