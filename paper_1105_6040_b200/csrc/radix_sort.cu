@@ -7,25 +7,32 @@
 // stable (equal keys keep input order, merge_sort's tie rule :77).
 //
 // Structure (one call, all on one stream, no host round trip):
-//   radix_prologue_kernel  one read of the keys: OR / OR-of-complement of all
+//   radix_prologue_all_kernel / radix_prologue_kernel
+//                          one read of the keys: OR / OR-of-complement of all
 //                          keys (which bits vary, hence which 8-bit digits are
-//                          constant and can be skipped) and the digit-0
-//                          histogram; zeroes look-back region 0.
+//                          constant and can be skipped), every digit's
+//                          histogram (4-byte keys; 8-byte keys: digit 0), a
+//                          sample of adjacent-pair order (structured input);
+//                          zeroes look-back region 0 when the first pass
+//                          uses it.
 //   radix_plan_kernel      1 thread: active digit list, histogram source per
 //                          slot, ping-pong buffer chain so the last executed
 //                          pass lands in the output.
-//   radix_fallback_hist    recounts the first active digit when digit 0 is
-//                          constant (exits at once otherwise).
-//   onesweep_kernel x S    one launch per digit slot: persistent CTAs scan the
-//                          slot's histogram into global digit offsets, take
-//                          tiles from an atomic counter, count digits per warp
-//                          (shared reductions), publish per-digit tile counts,
-//                          rank keys in-warp with ballot-based digit matching,
-//                          resolve the tile's global offsets by decoupled
-//                          look-back, stage the tile digit-sorted in shared
-//                          memory, write runs of equal digits with coalesced
-//                          stores, and count the NEXT slot's digit on the way
-//                          out (so no all-digit histogram pass is needed).
+//   radix_fallback_hist    recounts the first active digit when the prologue
+//                          did not count it (exits at once otherwise).
+//   onesweep_kernel x S    per digit slot, three kernels of which one runs it
+//                          (regular / skewed-pass / structured-input twins):
+//                          persistent CTAs scan the slot's histogram into
+//                          global digit offsets, take tiles from an atomic
+//                          counter (the next one streams in by TMA), rank keys
+//                          in-warp with lane-ordered shared atomics (ballot
+//                          matching where the device probe fails), publish
+//                          per-digit tile counts, resolve the tile's global
+//                          offsets by decoupled look-back (a keys-only sort's
+//                          first pass: fetch-and-add), stage the tile
+//                          digit-sorted in shared memory and write runs of
+//                          equal digits with coalesced stores; 8-byte keys
+//                          count the NEXT slot's digit on the way out.
 //   radix_copy_kernel      only does work when an in-place sort executed an
 //                          odd number of passes (or zero passes out of place).
 //
@@ -69,8 +76,9 @@ constexpr int kRadix = 256;
 #endif
 
 // kPrefetch: predecessors whose words are prefetched before the ranking. The
-// 64-bit words (n >= 2^30) prefetch one: two would push the static shared
-// memory past the two-CTAs-per-SM budget (2^31 i32 pass 7.8 ms at one CTA/SM).
+// 64-bit words (n > 2^31, see narrow_lookback_words) prefetch one: two would
+// push the static shared memory past the two-CTAs-per-SM budget (measured in
+// round 1 with 2^31 i32: 7.8 ms per pass at one CTA/SM).
 template <typename LB>
 struct LookbackWord;
 template <>
@@ -493,7 +501,7 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 // keys), so the layout minimises wavefronts: per-warp digit counters are
 // packed two 16-bit counters per word (a warp-tile count is <= 8192), ranks
 // are claimed by one shared atomic per digit group (the group's highest lane)
-// and broadcast with a shuffle, and global offsets are 32-bit when n < 2^30.
+// and broadcast with a shuffle, and global offsets are 32-bit when n <= 2^31.
 
 template <typename U, bool VALS, int THREADS, int ITEMS>
 struct OnesweepSmem {
@@ -665,7 +673,7 @@ struct TileShared {
 // steps read B2S_LB_STEP at a time (independent loads) in a warp-uniform loop.
 // The tile's inclusive prefix is published the moment it is known.
 // 32-bit words hold prefixes modulo 2^30; `lo` is a lower bound of the true
-// exclusive prefix less than 2^30 below it (see exclusive_floor), which makes
+// exclusive prefix less than 2^30 below it (narrow_lookback_words), which makes
 // the residue exact.
 template <typename LB>
 __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, LB* __restrict__ lb_cur,
