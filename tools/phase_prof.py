@@ -34,10 +34,6 @@ ctx.sort(keys, out=out)
 torch.cuda.synchronize()
 _lib.lib().b2s_debug_phase_cycles(buf, 1)
 tiles = (n + 12287) // 12288  # 512 x 24 u32 tiles
-print(f"look-back loop iterations per tile (warp 0): {buf[7] / (tiles * 4):.2f}; "
-      f"sync-step predecessors consumed {buf[6] % 1000000 / (tiles * 4):.2f}, "
-      f"unpublished hits {buf[6] // 1000000 / (tiles * 4):.2f}")
-buf[7] = buf[6] = 0
 for who, off in (("thread 0 (look-back warp)", 0), ("last thread", 8)):
     tot = sum(buf[off + k] for k in range(8)) or 1
     print(who + ": " + ", ".join(f"{NAMES[k]} {100 * buf[off + k] / tot:.1f}%" for k in range(6)))
