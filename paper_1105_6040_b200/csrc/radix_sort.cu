@@ -1331,6 +1331,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
     // a keys-only sort's first pass need not be stable: equal keys are
     // indistinguishable and no earlier pass's order is to be kept
     unsigned long long* const ticket = (!VALS && slot == 0 && B2S_TICKET_FIRST) ? ctr->ticket : nullptr;
+    const bool zero_next = slot + 1 < na;  // the last pass has no successor to zero words for
     const U* src = static_cast<const U*>(plan->ksrc[slot]);
     U* dst = static_cast<U*>(plan->kdst[slot]);
     const uint32_t* vsrc = plan->vsrc[slot];
@@ -1417,7 +1418,7 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         };
         const uint64_t tile_base = (uint64_t)tile * TILE;
         const uint64_t rem = n - tile_base;
-        if (tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;
+        if (zero_next && tid < kRadix) lb_next[(size_t)tile * kRadix + tid] = 0;  // the next slot's words
         uint32_t* idle = reinterpret_cast<uint32_t*>(kbuf[SEP ? 1 : cur ^ 1]);
         if (rem >= (uint64_t)TILE) {
             if (tma) {
