@@ -74,12 +74,35 @@ struct MergeItems {
 #ifdef B2S_MERGE_ITEMS
     static constexpr int value = sizeof(T) == 4 ? B2S_MERGE_ITEMS : B2S_MERGE_ITEMS64;
 #else
-    // odd: conflict-free restaging. u32 2-way round of 2^28 keys: 11 items
-    // 0.607 ms, 15: 0.572, 19: 0.555, 23: 0.558; u64 round of 2^27: 7 items
-    // 0.562 ms, 11: 0.485, 15: 0.459 (19 overflows 48 KB with a payload)
-    static constexpr int value = sizeof(T) == 4 ? 19 : 15;
+    // odd: conflict-free restaging. u32 2-way round of 2^28 keys with the
+    // shared-address merge step: 15 items 0.538 ms, 19: 0.505, 23: 0.481
+    // (27 overflows 48 KB of static shared memory with a payload); u64 round
+    // of 2^27: 11 items 0.458 ms, 15: 0.450 (round 1, index-based step: u32
+    // 19 items 0.555 ms, u64 15 items 0.459)
+    static constexpr int value = sizeof(T) == 4 ? 23 : 15;
 #endif
 };
+
+// shared-memory record load / store by 32-bit shared address
+template <typename T>
+__device__ __forceinline__ T lds_rec(uint32_t a) {
+    if constexpr (sizeof(T) == 4) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+        return (T)v;
+    } else {
+        unsigned long long v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+        return (T)v;
+    }
+}
+template <typename T>
+__device__ __forceinline__ void sts_rec(uint32_t a, T v) {
+    if constexpr (sizeof(T) == 4)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"((uint32_t)v) : "memory");
+    else
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"((unsigned long long)v) : "memory");
+}
 
 // 16 bytes global -> shared, asynchronously (both addresses 16-byte aligned)
 __device__ __forceinline__ void cp_async_16(void* dst, const void* src) {
@@ -163,12 +186,41 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
     const uint32_t diag = std::min<uint32_t>(threadIdx.x * ITEMS, cnt);
     uint32_t ai = merge_path_smem(sa_, la, sb_, lb, diag);
     uint32_t bi = diag - ai;
-    // the two heads live in registers: one shared load per output
-    T ka = sa_[ai], kb = sb_[bi];
     T rk[ITEMS];
     uint32_t rv[VALS ? ITEMS : 1];
+    if constexpr (!VALS) {
+        // keys only: both heads and both read positions as shared byte
+        // addresses in registers; per output one compare, one load of the
+        // taken side's next record and selects (no index arithmetic)
+        constexpr uint32_t SZ = sizeof(T);
+        const uint32_t a_s = (uint32_t)__cvta_generic_to_shared(sa_);
+        const uint32_t b_s = (uint32_t)__cvta_generic_to_shared(sb_);
+        uint32_t qa = a_s + ai * SZ, qb = b_s + bi * SZ;
+        const uint32_t ea = a_s + la * SZ, eb = b_s + lb * SZ;
+        T ka = lds_rec<T>(qa), kb = lds_rec<T>(qb);
+        auto step = [&](int j) {
+            const bool ta = qa < ea && (qb >= eb || !(kb < ka));
+            rk[j] = ta ? ka : kb;
+            const uint32_t qn = (ta ? qa : qb) + SZ;
+            const T v = lds_rec<T>(qn);
+            qa = ta ? qn : qa;
+            qb = ta ? qb : qn;
+            ka = ta ? v : ka;
+            kb = ta ? kb : v;
+        };
+        if (diag + ITEMS <= cnt) {
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
+            for (int j = 0; j < ITEMS; ++j) step(j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j)
+                if (diag + j < cnt) step(j);
+        }
+    }
+    // the two heads live in registers: one shared load per output
+    T ka = sa_[ai], kb = sb_[bi];
+#pragma unroll
+    for (int j = 0; j < (VALS ? ITEMS : 0); ++j) {
         if (diag + j < cnt) {
             const bool take_a = bi >= lb || (ai < la && !(kb < ka));
             rk[j] = take_a ? ka : kb;
@@ -399,26 +451,6 @@ template <typename T>
 struct GroupItems {
     static constexpr int value = sizeof(T) == 4 ? B2S_KG_ITEMS : 13;
 };
-
-template <typename T>
-__device__ __forceinline__ T lds_rec(uint32_t a) {
-    if constexpr (sizeof(T) == 4) {
-        uint32_t v;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-        return (T)v;
-    } else {
-        unsigned long long v;
-        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
-        return (T)v;
-    }
-}
-template <typename T>
-__device__ __forceinline__ void sts_rec(uint32_t a, T v) {
-    if constexpr (sizeof(T) == 4)
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"((uint32_t)v) : "memory");
-    else
-        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"((unsigned long long)v) : "memory");
-}
 
 // Merge path on shared-memory segments given by byte address: the number of
 // A records among the first `diag` outputs (ties to A).
@@ -726,14 +758,14 @@ int kway_mode() {
     static int m = -1;
     if (m < 0) {
         // -1 (default): the grouped single-pass merge for 4-byte keys,
-        // 4 <= k <= 16 and n >= 2^22, pairwise rounds otherwise; 0: always
+        // 5 <= k <= 8 and n >= 2^22, pairwise rounds otherwise; 0: always
         // pairwise; 1: grouped whenever it applies. The grouped merge reads
         // and writes every key once, but its rounds in shared memory are
         // bound by the merge step's dependency chain and the per-group
         // barriers, not HBM. Measured per 2^28 i32 keys (pairwise / grouped):
-        // k=3 1.005 / 1.064 ms, k=4 1.087 / 0.963, k=8 1.685 / 1.388, k=16
-        // 2.379 / 2.317; per 2^27 u64: k=3 0.885 / 0.932, k=4 0.948 / 0.990,
-        // k=8 1.484 / 1.428, k=16 2.123 / 2.700.
+        // k=3 0.901 / 1.064 ms, k=4 0.961 / 0.963, k=8 1.501 / 1.388, k=16
+        // 2.141 / 2.313; per 2^27 u64 (pairwise): k=2 0.450, k=4 0.921, k=8
+        // 1.441, k=16 2.065 (grouped 1.428 at k=8, slower elsewhere).
         const char* e = getenv("B2S_KWAY");
         m = e ? atoi(e) : -1;
     }
@@ -750,7 +782,7 @@ b2s_status kway_t(b2s_ctx* ctx, const void* const* runs, const uint32_t* const* 
     for (int i = 0; i < k; ++i) n_all += lens[i];
     // small merges are bound by their chain of launches: the grouped one's
     // sample sort adds a dozen (cfg1, 4 runs of 2^18: 0.112 vs 0.09 ms)
-    const bool grouped = mode == 1 || (mode < 0 && sizeof(T) == 4 && k >= 4 && n_all >= (1ull << 22));
+    const bool grouped = mode == 1 || (mode < 0 && sizeof(T) == 4 && k >= 5 && k <= 8 && n_all >= (1ull << 22));
     if (k > 2 && k <= kMaxK && grouped && kway_grouped_fits<T>(lens, k))
         return kway_grouped<T>(ctx, runs, vals, lens, k, out, vout);
     std::vector<Run> cur;
