@@ -1470,19 +1470,33 @@ __global__ void __launch_bounds__(THREADS, MINB) onesweep_kernel(RadixPlan* __re
         atomicAdd(&ctr->hist[slot + 1][tid], (unsigned long long)sh.nhist[tid]);
 }
 
+// n elements of T, 16-byte vectors where source and destination share their
+// 16-byte phase (the aligned middle), elements elsewhere
+template <typename T>
+__device__ __forceinline__ void copy_elems(const T* __restrict__ s, T* __restrict__ d, uint64_t n) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    constexpr uint32_t V = 16 / sizeof(T);
+    const uint32_t ps = (uint32_t)((reinterpret_cast<uintptr_t>(s) & 15) / sizeof(T));
+    const uint32_t pd = (uint32_t)((reinterpret_cast<uintptr_t>(d) & 15) / sizeof(T));
+    if (ps != pd) {
+        for (uint64_t i = tid; i < n; i += stride) d[i] = s[i];
+        return;
+    }
+    const uint64_t head = std::min<uint64_t>((V - ps) % V, n);
+    const uint64_t nv = (n - head) / V;
+    const uint4* __restrict__ sv = reinterpret_cast<const uint4*>(s + head);
+    uint4* __restrict__ dv = reinterpret_cast<uint4*>(d + head);
+    for (uint64_t i = tid; i < nv; i += stride) __stcs(dv + i, __ldcs(sv + i));
+    for (uint64_t i = tid; i < head; i += stride) d[i] = s[i];
+    for (uint64_t i = head + nv * V + tid; i < n; i += stride) d[i] = s[i];
+}
+
 template <typename U>
 __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n, int with_vals) {
     if (!plan->do_copy) return;
-    const U* __restrict__ s = static_cast<const U*>(plan->copy_ksrc);
-    U* __restrict__ d = static_cast<U*>(plan->copy_kdst);
-    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = tid; i < n; i += stride) d[i] = s[i];
-    if (with_vals) {
-        const uint32_t* __restrict__ vs = plan->copy_vsrc;
-        uint32_t* __restrict__ vd = plan->copy_vdst;
-        for (uint64_t i = tid; i < n; i += stride) vd[i] = vs[i];
-    }
+    copy_elems(static_cast<const U*>(plan->copy_ksrc), static_cast<U*>(plan->copy_kdst), n);
+    if (with_vals) copy_elems(plan->copy_vsrc, plan->copy_vdst, n);
 }
 
 // B2S_ALL_HIST: 1 (default) all-digit prologue for 4-byte keys, 2 also for
