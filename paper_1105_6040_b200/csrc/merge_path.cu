@@ -284,13 +284,6 @@ __global__ void __launch_bounds__(kMergeThreads) merge_tile_kernel(
 }
 
 template <typename T>
-__global__ void copy_kernel(const T* __restrict__ s, T* __restrict__ d, uint64_t n) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-        d[i] = s[i];
-}
-
-template <typename T>
 b2s_status copy_async(b2s_ctx* ctx, const T* s, T* d, uint64_t n) {
     if (n == 0 || s == d) return B2S_OK;
     B2S_CUDA(cudaMemcpyAsync(d, s, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
