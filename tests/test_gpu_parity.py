@@ -53,9 +53,10 @@ def test_quick_p4_gen_data_4096():
 
 def test_exhaustive_01():
     """P/tests/test_parallel_sort.cpp:314-328 (n <= 8) and acceptance
-    criterion 2's shape (P/tests/acceptance.cpp:160-189) at n <= 10."""
+    criterion 2 exactly (P/tests/acceptance.cpp:160-189): every 0/1 input of
+    n <= 12 keys at p in {2, 3, 4}, 24,573 sorts."""
     for p in (2, 3, 4):
-        for n in range(11):
+        for n in range(13):
             for mask in range(1 << n):
                 data = np.array([(mask >> i) & 1 for i in range(n)], dtype=np.int64)
                 out = sb.scatter_merge_sort(sb.Algorithm.bubble, data, opts(p)).sorted
