@@ -203,3 +203,14 @@ def test_verify_output_device_keys(dt):
     bad = good.flip(0)
     with pytest.raises(sb.VerificationError):
         sb.verify_output(inp, bad)
+
+
+@pytest.mark.parametrize("p", [16, 32, 64])
+def test_exp1_grid_largest_sizes(p):
+    """The exp1 grid's largest result-verified runs (P/tests/acceptance.cpp:
+    235-261): merge and quick at n = 600,000 with up to 64 processes, each
+    checked against the oracle as run_benchmark's verify_output does."""
+    data = oracle.gen_data(600_000, 1)
+    for algo in (sb.Algorithm.merge, sb.Algorithm.quick):
+        out = sb.scatter_merge_sort(algo, data, opts(p)).sorted
+        assert np.array_equal(np.asarray(out), oracle.sort(data)), (algo, p)
