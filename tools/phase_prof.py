@@ -1,6 +1,6 @@
 """Per-phase cycle split of the onesweep kernel (debug library from `make prof`).
 
-  B2S_LIB=paper_1105_6040_b200/lib/libb200sort_prof.so python tools/phase_prof.py [n] [uni|zipf|asc]
+  B2S_LIB=paper_1105_6040_b200/lib/libb200sort_prof.so python tools/phase_prof.py [n] [uni|zipf|asc|lo8|hi8]
 """
 import ctypes
 import os
@@ -21,6 +21,10 @@ if kind == "zipf":
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     from config_bench import zipf_keys
     keys = zipf_keys(ctx, n).view(torch.uint32)
+elif kind == "lo8":  # one active digit: a keys-only sort runs it as the ticket pass
+    keys = (ctx.gen_keys(n, 1, torch.uint32, shift=32).view(torch.int32) & 0xFF).view(torch.uint32)
+elif kind == "hi8":  # one active digit behind a payload-free ... (top digit only)
+    keys = (ctx.gen_keys(n, 1, torch.uint32, shift=32).view(torch.int32) & 0x7F000000).view(torch.uint32)
 elif kind == "asc":
     keys = torch.arange(n, dtype=torch.int32, device="cuda").view(torch.uint32)
 else:
