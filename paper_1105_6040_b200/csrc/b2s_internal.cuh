@@ -95,6 +95,8 @@ struct RadixPlan {
     int need_fallback;  // first active digit is not digit 0: recount it
     int structured;     // input nearly sorted either way: swizzled staging
     int all_hist;       // every digit's histogram came from the prologue (no in-pass counting)
+    int topfirst;       // 8-byte keys: only the upper four digits were sorted; the fix-up orders the ties
+    int fix_flag;       // set by the fix-up when a tie run is too long for it: the full sort follows
     int digit[kMaxSlots];
     uint32_t dxor[kMaxSlots];  // 0x80 on the top digit of signed keys
     const unsigned long long* hist[kMaxSlots];  // digit histogram per slot
@@ -113,6 +115,7 @@ struct RadixPlan {
 struct RadixCounters {
     unsigned long long hist[kMaxSlots][256];  // slot s's digit histogram
     unsigned long long spec0[256];            // prologue's digit-0 histogram
+    unsigned long long spec4[256];            // 8-byte keys, upper digits first: digit 4's histogram
     unsigned long long dhist[8][256];         // every digit's histogram (all-digit prologue)
     unsigned long long or_all;                // OR of all keys
     unsigned long long nor_all;               // OR of all complemented keys

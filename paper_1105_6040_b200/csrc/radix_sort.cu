@@ -35,6 +35,14 @@
 //                          count the NEXT slot's digit on the way out.
 //   radix_copy_kernel      only does work when an in-place sort executed an
 //                          odd number of passes (or zero passes out of place).
+//   topfirst_fixup_kernel  8-byte keys, 2^22..2^31 of them, whose upper half
+//                          varies in enough bits: only the four upper digits
+//                          are sorted (stable), which leaves ties of the upper
+//                          half -- a few percent of the keys, in runs of two or
+//                          three -- in input order; this kernel orders every
+//                          such run by its lower half (stable). A run it
+//                          cannot handle raises a flag and a second, full sort
+//                          (whose kernels all exit at once otherwise) follows.
 //
 // HBM traffic per executed pass: read + write of every key (and payload):
 // 2 * (key_bytes + val_bytes) * n. The prologue reads key_bytes * n once.
@@ -141,7 +149,7 @@ __device__ __forceinline__ void order_pairs(const U (&e)[D], uint32_t& asc, uint
     }
 }
 
-template <typename U, int D>
+template <typename U, int D, bool D4 = false>
 __device__ __forceinline__ void prologue_keys(const U (&e)[D], unsigned long long& o,
                                               unsigned long long& no, uint32_t hbase) {
 #pragma unroll
@@ -150,6 +158,11 @@ __device__ __forceinline__ void prologue_keys(const U (&e)[D], unsigned long lon
         no |= (unsigned long long)(U)~e[j];
         asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * ((uint32_t)e[j] & 0xFFu))
                      : "memory");
+        if constexpr (D4 && sizeof(U) == 8) {
+            // digit 4 (bits 32..39) into the second histogram, 1 KB further
+            const uint32_t d4 = (uint32_t)((unsigned long long)e[j] >> 32) & 0xFFu;
+            asm volatile("red.shared.add.u32 [%0+1024], 1;" ::"r"(hbase + 4u * d4) : "memory");
+        }
     }
 }
 
@@ -158,16 +171,18 @@ __device__ __forceinline__ void prologue_keys(const U (&e)[D], unsigned long lon
 template <typename U>
 constexpr int kPrologueMinBlocks = sizeof(U) == 4 ? 4 : 3;
 
-template <typename U>
+template <typename U, bool D4 = false>
 __global__ void __launch_bounds__(512, kPrologueMinBlocks<U>) radix_prologue_kernel(const U* __restrict__ keys, uint64_t n,
                                                              RadixCounters* __restrict__ ctr,
                                                              uint4* __restrict__ lb_zero,
-                                                             uint64_t lb_zero_vecs) {
+                                                             uint64_t lb_zero_vecs,
+                                                             const RadixPlan* __restrict__ cond) {
     constexpr int VEC = 16 / sizeof(U);
-    __shared__ uint32_t s_h[kRadix];
+    if (cond != nullptr && cond->fix_flag == 0) return;  // the conditional full sort is not needed
+    __shared__ uint32_t s_h[D4 ? 2 * kRadix : kRadix];  // digit 0 | digit 4
     __shared__ unsigned long long s_or[16], s_nor[16];
     __shared__ uint2 s_ord[16];
-    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) s_h[i] = 0;
+    for (int i = threadIdx.x; i < (D4 ? 2 : 1) * kRadix; i += blockDim.x) s_h[i] = 0;
     __syncthreads();
     const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(s_h);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -188,19 +203,19 @@ __global__ void __launch_bounds__(512, kPrologueMinBlocks<U>) radix_prologue_ker
             for (int u = 0; u < 4; ++u) q[u] = __ldcs(kv + v + u * stride);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                prologue_keys<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q[u]), o, no, hbase);
+                prologue_keys<U, VEC, D4>(*reinterpret_cast<const U(*)[VEC]>(&q[u]), o, no, hbase);
             order_pairs<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q[0]), asc, desc);
         }
         for (; v < nvec; v += stride) {
             uint4 q = __ldcs(kv + v);
-            prologue_keys<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q), o, no, hbase);
+            prologue_keys<U, VEC, D4>(*reinterpret_cast<const U(*)[VEC]>(&q), o, no, hbase);
             order_pairs<U, VEC>(*reinterpret_cast<const U(*)[VEC]>(&q), asc, desc);
         }
         head = nvec * VEC;
     }
     for (uint64_t i = head + tid; i < n; i += stride) {
         const U e[1] = {keys[i]};
-        prologue_keys<U, 1>(e, o, no, hbase);
+        prologue_keys<U, 1, D4>(e, o, no, hbase);
     }
     // block OR-reduction, then one global atomic per block
 #pragma unroll
@@ -233,6 +248,10 @@ __global__ void __launch_bounds__(512, kPrologueMinBlocks<U>) radix_prologue_ker
     for (int i = threadIdx.x; i < kRadix; i += blockDim.x) {
         const uint32_t c = s_h[i];
         if (c) atomicAdd(&ctr->spec0[i], (unsigned long long)c);
+        if constexpr (D4) {
+            const uint32_t c4 = s_h[kRadix + i];
+            if (c4) atomicAdd(&ctr->spec4[i], (unsigned long long)c4);
+        }
     }
 }
 
@@ -256,8 +275,10 @@ template <typename U>
 __global__ void __launch_bounds__(kAllHistThreads, 1)
     radix_prologue_all_kernel(const U* __restrict__ keys, uint64_t n,
                               RadixCounters* __restrict__ ctr, uint4* __restrict__ lb_zero,
-                              uint64_t lb_zero_vecs, uint32_t top_xor) {
+                              uint64_t lb_zero_vecs, uint32_t top_xor,
+                              const RadixPlan* __restrict__ cond) {
     constexpr int ND = sizeof(U);            // digits
+    if (cond != nullptr && cond->fix_flag == 0) return;
     constexpr int COLS = sizeof(U) == 4 ? 32 : 16;
     constexpr int VEC = 16 / sizeof(U);      // keys per 16-byte load
     static_assert((size_t)ND * 256 * COLS * 4 == kAllHistSmem, "column layout");
@@ -377,14 +398,41 @@ __global__ void __launch_bounds__(kAllHistThreads, 1)
 __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* __restrict__ ctr,
                                   int np, uint64_t n, uint32_t top_xor, const void* kin,
                                   void* kout, void* ktmp, const uint32_t* vin, uint32_t* vout,
-                                  uint32_t* vtmp, int all_hist) {
+                                  uint32_t* vtmp, int all_hist, int top_mode,
+                                  const RadixPlan* __restrict__ cond) {
     if (threadIdx.x < kMaxSlots) plan->tile_counter[threadIdx.x] = 0;
     if (threadIdx.x != 0) return;
+    plan->topfirst = 0;
+    plan->fix_flag = 0;
+    if (top_mode == 2 && cond->fix_flag == 0) {  // the fix-up finished the sort: nothing to do
+        plan->num_active = 0;
+        plan->do_copy = 0;
+        plan->need_fallback = 0;
+        plan->structured = 0;
+        plan->all_hist = 0;
+        return;
+    }
     // a bit varies iff some key has it set and some key has it clear
     const unsigned long long varying = ctr->or_all & ctr->nor_all;
+    // Upper-digits-first (top_mode 1, 8-byte keys): with b varying bits in the
+    // upper half, n keys fall into ~2^b classes of equal upper halves; from
+    // b >= log2(n) + 2 on at most ~1/8 of the keys share their class, in runs
+    // of two or three, which the fix-up kernel orders. The four lower passes
+    // are then not run at all.
+    unsigned int dmask = 0xFFu;
+    if (top_mode == 1) {
+        const int hi_bits = __popcll(varying >> 32), lo_bits = __popcll(varying & 0xFFFFFFFFull);
+        int need = 2;
+        while (need - 2 < 62 && (1ull << (need - 2)) < n) ++need;  // ceil(log2 n) + 2
+        if (lo_bits > 0 && hi_bits >= (need < 32 ? need : 32)) {
+            dmask = 0xF0u;
+            plan->topfirst = 1;
+        }
+    }
     int na = 0;
     for (int p = 0; p < np && n > 0; ++p) {
         if (((varying >> (8 * p)) & 0xFFull) == 0) continue;  // constant digit: identity pass
+        if (((dmask >> p) & 1u) == 0) continue;               // left to the fix-up
         plan->digit[na] = p;
         plan->dxor[na] = (p == np - 1) ? top_xor : 0u;
         plan->hist[na] = all_hist ? ctr->dhist[p] : ctr->hist[na];
@@ -402,6 +450,10 @@ __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* _
     plan->all_hist = all_hist;
     plan->need_fallback = !all_hist && (na > 0 && plan->digit[0] != 0);
     if (!all_hist && na > 0 && plan->digit[0] == 0) plan->hist[0] = ctr->spec0;
+    if (!all_hist && top_mode == 1 && na > 0 && plan->digit[0] == 4) {  // counted by the prologue too
+        plan->hist[0] = ctr->spec4;
+        plan->need_fallback = 0;
+    }
     // Buffer chain: slot s writes `out` when (na-1-s) is even, else `tmp`, so
     // the last executed slot always lands in `out`. When in == out and na is
     // odd, slot 0 cannot write `out` (it is reading it): the chain then runs
@@ -1499,6 +1551,139 @@ __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n
     if (with_vals) copy_elems(plan->copy_vsrc, plan->copy_vdst, n);
 }
 
+// Orders the ties of an upper-digits-first sort (see radix_plan_kernel): the
+// array is sorted (stably) by the keys' upper halves; the thread at the first
+// element of a run of equal upper halves walks the run and, when its lower
+// halves are not already ascending, sorts it in place by insertion (stable;
+// payloads move with their keys). Only the run's owner writes it, and what the
+// other threads read of it -- upper halves -- does not change. Runs longer
+// than kFixScan, or unsorted ones longer than kFixSort, raise plan->fix_flag.
+constexpr uint32_t kFixScan = 4096, kFixSort = 32;
+
+// One tie run starting at element i (see topfirst_fixup_kernel).
+template <bool VALS>
+__device__ __noinline__ void fixup_run(RadixPlan* plan, unsigned long long* keys, uint32_t* vals,
+                                       uint64_t n, uint64_t i) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(keys);  // w[2i]: lower half, w[2i+1]: upper
+    {
+        // runs of two, nearly all of them: three independent loads, at most one swap
+        const unsigned long long k0 = keys[i], k1 = keys[i + 1];
+        const unsigned long long k2 = i + 2 < n ? keys[i + 2] : ~k0;
+        if ((uint32_t)(k2 >> 32) != (uint32_t)(k0 >> 32)) {
+            if ((uint32_t)k0 > (uint32_t)k1) {
+                keys[i] = k1;
+                keys[i + 1] = k0;
+                if constexpr (VALS) {
+                    const uint32_t v0 = vals[i], v1 = vals[i + 1];
+                    vals[i] = v1;
+                    vals[i + 1] = v0;
+                }
+            }
+            return;
+        }
+    }
+    const uint32_t hi = w[2 * i + 1];
+    uint64_t j = i + 1;
+    uint32_t prev = w[2 * i];
+    bool sorted = true, ended = false;
+    while (j < n && j - i < kFixScan) {
+        if (w[2 * j + 1] != hi) {
+            ended = true;
+            break;
+        }
+        const uint32_t lo = w[2 * j];
+        sorted = sorted && prev <= lo;
+        prev = lo;
+        ++j;
+    }
+    if (!ended && j < n && w[2 * j + 1] == hi) {  // longer than the scan window
+        plan->fix_flag = 1;
+        return;
+    }
+    if (sorted) return;
+    const uint32_t len = (uint32_t)(j - i);
+    if (len > kFixSort) {
+        plan->fix_flag = 1;
+        return;
+    }
+    for (uint32_t a = 1; a < len; ++a) {
+        const unsigned long long x = keys[i + a];
+        uint32_t vx = 0;
+        if constexpr (VALS) vx = vals[i + a];
+        uint32_t b = a;
+        while (b > 0 && (uint32_t)keys[i + b - 1] > (uint32_t)x) {
+            keys[i + b] = keys[i + b - 1];
+            if constexpr (VALS) vals[i + b] = vals[i + b - 1];
+            --b;
+        }
+        keys[i + b] = x;
+        if constexpr (VALS) vals[i + b] = vx;
+    }
+}
+
+// Each lane reads four consecutive keys (two 16-byte loads) per step and gets
+// its neighbours' boundary upper halves by shuffle; the lanes that find a run
+// start (upper half differs from the predecessor's and equals the
+// successor's) handle their runs.
+template <bool VALS>
+__global__ void __launch_bounds__(256) topfirst_fixup_kernel(RadixPlan* __restrict__ plan,
+                                                             unsigned long long* keys, uint32_t* vals,
+                                                             uint64_t n) {
+    if (!plan->topfirst) return;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(keys);
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    if ((reinterpret_cast<uintptr_t>(keys) & 15) != 0) {  // unaligned: one element per thread
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n; i += stride) {
+            const uint32_t hi = w[2 * i + 1];
+            if (w[2 * i + 3] == hi && (i == 0 || w[2 * i - 1] != hi)) fixup_run<VALS>(plan, keys, vals, n, i);
+        }
+        return;
+    }
+    const uint4* kv = reinterpret_cast<const uint4*>(keys);
+    for (uint64_t base = warp * 128; base < n; base += nwarps * 128) {  // warp-uniform trips
+        const uint64_t i0 = base + 4 * (uint64_t)lane;
+        uint32_t t[6];  // upper halves of elements i0-1 .. i0+4 (0/1 sentinels past the ends)
+        uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+        if (i0 + 1 < n) a = kv[i0 / 2];
+        else if (i0 < n) a.y = w[2 * i0 + 1];
+        if (i0 + 3 < n) b = kv[i0 / 2 + 1];
+        else if (i0 + 2 < n) b.y = w[2 * (i0 + 2) + 1];
+        t[1] = a.y;
+        t[2] = a.w;
+        t[3] = b.y;
+        t[4] = b.w;
+        const uint32_t up = __shfl_up_sync(0xffffffffu, t[4], 1);
+        const uint32_t dn = __shfl_down_sync(0xffffffffu, t[1], 1);
+        t[0] = lane > 0 ? up : (i0 > 0 ? w[2 * i0 - 1] : ~t[1]);
+        t[5] = lane < 31 ? dn : (i0 + 4 < n ? w[2 * (i0 + 4) + 1] : 0u);
+        uint32_t starts = 0;  // bit e: element i0 + e opens a run
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint64_t i = i0 + e;
+            if (i + 1 < n && t[e + 1] == t[e + 2] && (i == 0 || t[e] != t[e + 1])) starts |= 1u << e;
+        }
+        while (starts) {  // one call site: the lanes with a run handle theirs together
+            const int e = __ffs(starts) - 1;
+            starts &= starts - 1;
+            fixup_run<VALS>(plan, keys, vals, n, i0 + e);
+        }
+    }
+}
+
+// B2S_TOPFIRST=0 turns the upper-digits-first path of 8-byte keys off
+bool topfirst_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("B2S_TOPFIRST");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+constexpr uint64_t kTopFirstMinKeys = 1ull << 22, kTopFirstMaxKeys = 1ull << 31;
+
 // B2S_ALL_HIST: 1 (default) all-digit prologue for 4-byte keys, 2 also for
 // 8-byte keys, 0 never (each next digit is counted inside the passes)
 int all_hist_mode() {
@@ -1655,7 +1840,11 @@ bool narrow_lookback_words(uint64_t n, uint64_t tile) {
 
 template <typename U, bool VALS>
 b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kout,
-                        const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc) {
+                        const uint32_t* vin, uint32_t* vout, uint64_t n, const SortScratch* sc,
+                        int top_mode = 0) {
+    // top_mode (own scratch only): 0 the plain sort; 1 the upper digits first
+    // when the plan kernel finds the keys fit (plan[0]); 2 the full sort that
+    // runs only if the fix-up raised plan[0].fix_flag (plan[1])
     constexpr int NP = sizeof(U);
     const uint32_t top_xor = is_signed ? 0x80u : 0u;
     const size_t lb_region = lookback_region_bytes(n, (int)sizeof(U), VALS);
@@ -1665,12 +1854,13 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
         B2S_TRY(ctx->alt_keys.ensure(n * sizeof(U)));
         if (VALS) B2S_TRY(ctx->alt_vals.ensure(n * 4));
         B2S_TRY(ctx->lookback.ensure(2 * lb_region + 16));
-        B2S_TRY(ctx->plan.ensure(sizeof(RadixPlan)));
+        B2S_TRY(ctx->plan.ensure(2 * sizeof(RadixPlan)));
         own = {ctx->alt_keys.ptr, static_cast<uint32_t*>(ctx->alt_vals.ptr), ctx->lookback.ptr,
                static_cast<RadixCounters*>(ctx->hist.ptr), static_cast<RadixPlan*>(ctx->plan.ptr)};
         sc = &own;
     }
-    RadixPlan* plan = sc->plan;
+    const RadixPlan* cond = top_mode == 2 ? sc->plan : nullptr;
+    RadixPlan* plan = sc->plan + (top_mode == 2 ? 1 : 0);
     RadixCounters* ctr = sc->ctr;
     const bool wide = !narrow_lookback_words(n, lookback_tile(n, (int)sizeof(U), VALS));
     ctx->ev_hist0 = record(ctx);
@@ -1693,20 +1883,26 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
         // runs without look-back (tickets): nothing to zero then
         const size_t zero16 = (!VALS && B2S_TICKET_FIRST) ? 0 : (lb_region + 15) / 16;
         radix_prologue_all_kernel<U><<<grid, kAllHistThreads, kAllHistSmem, ctx->stream>>>(
-            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback), zero16, top_xor);
+            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback), zero16, top_xor, cond);
         B2S_LAUNCHED();
     } else {
         const int threads = 512;
         uint64_t want = (n / (16 / sizeof(U)) + threads - 1) / threads;
         int grid = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1),
                                            (uint64_t)ctx->num_sms * kPrologueMinBlocks<U>);
-        radix_prologue_kernel<U><<<grid, threads, 0, ctx->stream>>>(
-            static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
-            (lb_region + 15) / 16);
+        if (top_mode == 1 && sizeof(U) == 8)
+            radix_prologue_kernel<U, true><<<grid, threads, 0, ctx->stream>>>(
+                static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
+                (lb_region + 15) / 16, cond);
+        else
+            radix_prologue_kernel<U><<<grid, threads, 0, ctx->stream>>>(
+                static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
+                (lb_region + 15) / 16, cond);
         B2S_LAUNCHED();
     }
     radix_plan_kernel<<<1, 32, 0, ctx->stream>>>(plan, ctr, NP, n, top_xor, kin, kout,
-                                                 sc->alt_keys, vin, vout, sc->alt_vals, all_hist ? 1 : 0);
+                                                 sc->alt_keys, vin, vout, sc->alt_vals, all_hist ? 1 : 0,
+                                                 top_mode, cond);
     B2S_LAUNCHED();
     if (n > 0 && !all_hist) {  // the all-digit prologue needs no recount
         int grid = (int)std::min<uint64_t>((n + 511) / 512, (uint64_t)ctx->num_sms * 4);
@@ -1822,8 +2018,40 @@ b2s_status radix_sort(b2s_ctx* ctx, b2s_dtype dtype, const void* kin, void* kout
         return vals ? radix_sort_t<uint32_t, true>(ctx, sgn, kin, kout, vin, vout, n, sc)
                     : radix_sort_t<uint32_t, false>(ctx, sgn, kin, kout, vin, vout, n, sc);
     }
-    return vals ? radix_sort_t<unsigned long long, true>(ctx, sgn, kin, kout, vin, vout, n, sc)
-                : radix_sort_t<unsigned long long, false>(ctx, sgn, kin, kout, vin, vout, n, sc);
+    using K = unsigned long long;
+    // upper digits first (radix_plan_kernel decides on the device whether the
+    // keys fit; if not, this first sort is the plain one and the rest no-ops)
+    const bool top = sc == nullptr && n >= kTopFirstMinKeys && n <= kTopFirstMaxKeys && topfirst_enabled();
+    if (!top) {
+        return vals ? radix_sort_t<K, true>(ctx, sgn, kin, kout, vin, vout, n, sc)
+                    : radix_sort_t<K, false>(ctx, sgn, kin, kout, vin, vout, n, sc);
+    }
+    B2S_TRY(vals ? (radix_sort_t<K, true>(ctx, sgn, kin, kout, vin, vout, n, nullptr, 1))
+                 : (radix_sort_t<K, false>(ctx, sgn, kin, kout, vin, vout, n, nullptr, 1)));
+    RadixPlan* plan = static_cast<RadixPlan*>(ctx->plan.ptr);
+    {
+        const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+        if (vals)
+            topfirst_fixup_kernel<true><<<grid, 256, 0, ctx->stream>>>(plan, static_cast<K*>(kout), vout, n);
+        else
+            topfirst_fixup_kernel<false><<<grid, 256, 0, ctx->stream>>>(plan, static_cast<K*>(kout), vout, n);
+        B2S_LAUNCHED();
+    }
+    // the conditional full sort, in place; the timing keeps the first sort's
+    // events (its passes are the ones that normally run) and ends after it
+    const bool timing = ctx->timing;
+    const int e_h0 = ctx->ev_hist0, e_h1 = ctx->ev_hist1;
+    int e_pass[kMaxSlots + 1];
+    for (int s = 0; s <= kMaxSlots; ++s) e_pass[s] = ctx->ev_pass[s];
+    ctx->timing = false;
+    const b2s_status st = vals ? radix_sort_t<K, true>(ctx, sgn, kout, kout, vout, vout, n, nullptr, 2)
+                               : radix_sort_t<K, false>(ctx, sgn, kout, kout, vout, vout, n, nullptr, 2);
+    ctx->timing = timing;
+    ctx->ev_hist0 = e_h0;
+    ctx->ev_hist1 = e_h1;
+    for (int s = 0; s <= kMaxSlots; ++s) ctx->ev_pass[s] = e_pass[s];
+    ctx->ev_copy1 = record(ctx);
+    return st;
 }
 
 }  // namespace b2s
