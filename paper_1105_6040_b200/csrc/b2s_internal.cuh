@@ -91,7 +91,7 @@ enum { kMaxSlots = 8 };
 // num_active exit at once.
 struct RadixPlan {
     int num_active;
-    int do_copy;
+    int do_copy;        // 1: copy (in-place odd pass count / zero passes out of place), 2: reversed
     int need_fallback;  // first active digit is not digit 0: recount it
     int structured;     // input nearly sorted either way: swizzled staging
     int all_hist;       // every digit's histogram came from the prologue (no in-pass counting)
@@ -120,6 +120,8 @@ struct RadixCounters {
     unsigned long long or_all;                // OR of all keys
     unsigned long long nor_all;               // OR of all complemented keys
     unsigned long long asc_pairs, desc_pairs;  // sampled adjacent pairs in order / reversed
+    // every adjacent pair, counted by radix_order_check_kernel when the sample is all one way
+    unsigned long long gt_pairs, lt_pairs, order_checked;
     unsigned long long ticket[256];            // keys-only first pass: digit offsets in tile arrival order
 };
 

@@ -15,6 +15,14 @@
 //                          sample of adjacent-pair order (structured input);
 //                          zeroes look-back region 0 when the first pass
 //                          uses it.
+//   radix_order_check_kernel  when the prologue's sample of adjacent pairs is
+//                          all one way (and some bit varies): counts every
+//                          adjacent pair k[i] > k[i+1] and k[i] < k[i+1]; an
+//                          ascending input then runs no pass at all (copied
+//                          if out of place), a descending one is reversed
+//                          (keys only: non-increasing; with a payload:
+//                          strictly decreasing, so the order stays stable).
+//                          Exits at once otherwise.
 //   radix_plan_kernel      1 thread: active digit list, histogram source per
 //                          slot, ping-pong buffer chain so the last executed
 //                          pass lands in the output.
@@ -393,6 +401,73 @@ __global__ void __launch_bounds__(kAllHistThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// exact order check of presorted-looking input
+constexpr uint64_t kOrderCheckMinKeys = 1ull << 20;
+
+template <typename U>
+__global__ void __launch_bounds__(512) radix_order_check_kernel(const U* __restrict__ keys, uint64_t n,
+                                                                 RadixCounters* __restrict__ ctr,
+                                                                 U flip) {
+    // gate: the sampled pairs (raw unsigned compare; a signed array crossing
+    // zero shows one odd pair) are all one way, and the keys are not all equal
+    {
+        const unsigned long long a = ctr->asc_pairs, d = ctr->desc_pairs;
+        if ((a < d ? a : d) > 2 || (ctr->or_all & ctr->nor_all) == 0) return;
+    }
+    constexpr int VEC = 16 / sizeof(U);
+    const int lane = threadIdx.x & 31;
+    unsigned long long gt = 0, lt = 0;
+    auto cmp = [&](U x, U y) {  // x before y in the input
+        x ^= flip;
+        y ^= flip;
+        gt += x > y;
+        lt += x < y;
+    };
+    if ((reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
+        const uint4* kv = reinterpret_cast<const uint4*>(keys);
+        const uint64_t nvec = n / VEC;
+        const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+        const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+        for (uint64_t v0 = warp * 32; v0 < nvec; v0 += nwarps * 32) {  // warp-uniform trips
+            const uint64_t v = v0 + lane;
+            uint4 q = make_uint4(0, 0, 0, 0);
+            if (v < nvec) q = __ldcs(kv + v);
+            const U(&e)[VEC] = *reinterpret_cast<const U(*)[VEC]>(&q);
+            // the next vector's first element: the next lane's, or one load
+            U nxt;
+            if constexpr (sizeof(U) == 4) {
+                nxt = (U)__shfl_down_sync(0xffffffffu, (uint32_t)e[0], 1);
+            } else {
+                nxt = (U)__shfl_down_sync(0xffffffffu, (unsigned long long)e[0], 1);
+            }
+            if (v < nvec) {
+#pragma unroll
+                for (int j = 0; j + 1 < VEC; ++j) cmp(e[j], e[j + 1]);
+                const uint64_t ni = (v + 1) * VEC;
+                if (ni < n) cmp(e[VEC - 1], (lane < 31 && v + 1 < nvec) ? nxt : keys[ni]);
+            }
+        }
+        // the tail after the last whole vector
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            for (uint64_t i = nvec * VEC; i + 1 < n; ++i) cmp(keys[i], keys[i + 1]);
+    } else {
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n; i += stride)
+            cmp(keys[i], keys[i + 1]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        gt += __shfl_xor_sync(0xffffffffu, gt, off);
+        lt += __shfl_xor_sync(0xffffffffu, lt, off);
+    }
+    if (lane == 0) {
+        if (gt) atomicAdd(&ctr->gt_pairs, gt);
+        if (lt) atomicAdd(&ctr->lt_pairs, lt);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->order_checked = 1;
+}
+
+// ---------------------------------------------------------------------------
 // pass plan: active digits, histogram per slot, buffer chain
 
 __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* __restrict__ ctr,
@@ -438,6 +513,19 @@ __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* _
         plan->hist[na] = all_hist ? ctr->dhist[p] : ctr->hist[na];
         ++na;
     }
+    // presorted input (radix_order_check_kernel counted every adjacent pair):
+    // ascending runs no pass; descending (with a payload: strictly) is reversed
+    bool reversed = false;
+    if (top_mode != 2 && ctr->order_checked && n > 1) {
+        const unsigned long long gt = ctr->gt_pairs, lt = ctr->lt_pairs;
+        if (gt == 0) {
+            na = 0;
+        } else if (vin != nullptr ? gt == n - 1 : lt == 0) {
+            na = 0;
+            reversed = true;
+        }
+        if (na == 0) plan->topfirst = 0;
+    }
     plan->num_active = na;
     // structured input (sorted, reverse, nearly so): adjacent pairs almost all
     // in one direction. Its passes scatter with strided slots, so they run
@@ -475,7 +563,11 @@ __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* _
         vsrc = vdst;
     }
     plan->do_copy = 0;
-    if (na == 0 && !in_place) {
+    if (reversed) {
+        plan->do_copy = 2;
+        plan->copy_ksrc = kin;
+        plan->copy_vsrc = vin;
+    } else if (na == 0 && !in_place) {
         plan->do_copy = 1;
         plan->copy_ksrc = kin;
         plan->copy_vsrc = vin;
@@ -1544,9 +1636,57 @@ __device__ __forceinline__ void copy_elems(const T* __restrict__ s, T* __restric
     for (uint64_t i = head + nv * V + tid; i < n; i += stride) d[i] = s[i];
 }
 
+template <typename T>
+__device__ __forceinline__ uint4 reverse_vec(uint4 q) {
+    if constexpr (sizeof(T) == 4) return make_uint4(q.w, q.z, q.y, q.x);
+    else return make_uint4(q.z, q.w, q.x, q.y);
+}
+
+// d[i] = s[n-1-i]; s == d reverses in place. 16-byte vectors when n is a whole
+// number of them and both arrays are aligned, elements otherwise.
+template <typename T>
+__device__ __forceinline__ void reverse_elems(const T* s, T* d, uint64_t n) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    constexpr uint32_t V = 16 / sizeof(T);
+    const bool vec = n % V == 0 && ((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0;
+    if (s != d) {
+        if (vec) {
+            const uint64_t nv = n / V;
+            const uint4* sv = reinterpret_cast<const uint4*>(s);
+            uint4* dv = reinterpret_cast<uint4*>(d);
+            for (uint64_t i = tid; i < nv; i += stride) __stcs(dv + (nv - 1 - i), reverse_vec<T>(__ldcs(sv + i)));
+        } else {
+            for (uint64_t i = tid; i < n; i += stride) d[n - 1 - i] = s[i];
+        }
+        return;
+    }
+    if (vec) {
+        const uint64_t nv = n / V;
+        uint4* dv = reinterpret_cast<uint4*>(d);
+        for (uint64_t i = tid; i < (nv + 1) / 2; i += stride) {
+            const uint64_t j = nv - 1 - i;
+            const uint4 a = dv[i], b = dv[j];
+            dv[j] = reverse_vec<T>(a);
+            if (i != j) dv[i] = reverse_vec<T>(b);
+        }
+    } else {
+        for (uint64_t i = tid; i < n / 2; i += stride) {
+            const T a = d[i], b = d[n - 1 - i];
+            d[i] = b;
+            d[n - 1 - i] = a;
+        }
+    }
+}
+
 template <typename U>
 __global__ void radix_copy_kernel(const RadixPlan* __restrict__ plan, uint64_t n, int with_vals) {
     if (!plan->do_copy) return;
+    if (plan->do_copy == 2) {
+        reverse_elems(static_cast<const U*>(plan->copy_ksrc), static_cast<U*>(plan->copy_kdst), n);
+        if (with_vals) reverse_elems(plan->copy_vsrc, plan->copy_vdst, n);
+        return;
+    }
     copy_elems(static_cast<const U*>(plan->copy_ksrc), static_cast<U*>(plan->copy_kdst), n);
     if (with_vals) copy_elems(plan->copy_vsrc, plan->copy_vdst, n);
 }
@@ -1898,6 +2038,12 @@ b2s_status radix_sort_t(b2s_ctx* ctx, bool is_signed, const void* kin, void* kou
             radix_prologue_kernel<U><<<grid, threads, 0, ctx->stream>>>(
                 static_cast<const U*>(kin), n, ctr, static_cast<uint4*>(sc->lookback),
                 (lb_region + 15) / 16, cond);
+        B2S_LAUNCHED();
+    }
+    if (n >= kOrderCheckMinKeys && top_mode != 2) {
+        const U flip = is_signed ? (U)1 << (8 * sizeof(U) - 1) : (U)0;
+        const int grid = (int)std::min<uint64_t>((n / (16 / sizeof(U)) + 511) / 512, (uint64_t)ctx->num_sms * 4);
+        radix_order_check_kernel<U><<<std::max(grid, 1), 512, 0, ctx->stream>>>(static_cast<const U*>(kin), n, ctr, flip);
         B2S_LAUNCHED();
     }
     radix_plan_kernel<<<1, 32, 0, ctx->stream>>>(plan, ctr, NP, n, top_xor, kin, kout,
