@@ -91,13 +91,18 @@ constexpr int kRadix = 256;
 #endif
 
 #ifndef B2S_LB_PRE
-#define B2S_LB_PRE 2  // measured per 2^28 u32 pass: 2: 0.719 ms, 4: 0.723, 8: 0.98 (smem)
+// predecessors' words prefetched (cp.async) before the ranking. Round 1: 2:
+// 0.719 ms per 2^28 u32 pass, 4: 0.723, 8: 0.98 (smem). With the current
+// kernel only 1.5% of the look-backs finish from the prefetched words (the
+// predecessors have not published yet), and none is better: 0: 0.673 ms,
+// 1: 0.676, 2: 0.681 (cfg3 22.56 -> 22.25 ms, cfg5's passes 1.855 -> 1.818)
+#define B2S_LB_PRE 0
 #endif
 
 // kPrefetch: predecessors whose words are prefetched before the ranking. The
-// 64-bit words (n > 2^31, see narrow_lookback_words) prefetch one: two would
-// push the static shared memory past the two-CTAs-per-SM budget (measured in
-// round 1 with 2^31 i32: 7.8 ms per pass at one CTA/SM).
+// 64-bit words (n > 2^31, see narrow_lookback_words) prefetch at most one: two
+// would push the static shared memory past the two-CTAs-per-SM budget
+// (measured in round 1 with 2^31 i32: 7.8 ms per pass at one CTA/SM).
 template <typename LB>
 struct LookbackWord;
 template <>
@@ -110,7 +115,7 @@ template <>
 struct LookbackWord<unsigned long long> {
     static constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62,
                                         kMask = (1ull << 62) - 1;
-    static constexpr int kPrefetch = 1;
+    static constexpr int kPrefetch = B2S_LB_PRE ? 1 : 0;
     static __device__ __forceinline__ unsigned long long flag(unsigned long long w) {
         return w >> 62;
     }
@@ -808,7 +813,7 @@ struct TileShared {
     uint32_t start[kRadix];
     uint32_t wsum[kRadix / 32];
     unsigned long long wsum64[kRadix / 32];
-    alignas(16) LB lbw[LookbackWord<LB>::kPrefetch * kRadix];  // prefetched look-back window
+    alignas(16) LB lbw[LookbackWord<LB>::kPrefetch > 0 ? LookbackWord<LB>::kPrefetch * kRadix : 4];  // prefetched look-back window
     uint32_t tile[2];
     uint32_t dummy[32];  // sink of the non-leaders' no-op rank atomics
     alignas(8) unsigned long long mbar[2];

@@ -29,7 +29,11 @@ for kind in os.environ.get("KDEV_KINDS", "uni,skew,asc").split(","):
         k = ctx.gen_keys(n, 2, torch.uint32, shift=32).view(torch.int32)
         keys = (k & (k >> 3) & (k >> 7)).view(torch.uint32)   # bits biased to 0: skewed digits
     else:
-        keys = torch.arange(n, dtype=torch.int32, device="cuda").view(torch.uint32)
+        # ascending but for one swapped pair, so the passes (structured twin)
+        # run instead of the presorted shortcut
+        k = torch.arange(n, dtype=torch.int32, device="cuda")
+        k[:2] = torch.tensor([1, 0], dtype=torch.int32, device="cuda")
+        keys = k.view(torch.uint32)
     out = torch.empty_like(keys)
     ctx.enable_timing(True)
     ps, tot = [], []
