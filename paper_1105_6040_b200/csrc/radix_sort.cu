@@ -504,7 +504,11 @@ __global__ void radix_plan_kernel(RadixPlan* __restrict__ plan, RadixCounters* _
         const int hi_bits = __popcll(varying >> 32), lo_bits = __popcll(varying & 0xFFFFFFFFull);
         int need = 2;
         while (need - 2 < 62 && (1ull << (need - 2)) < n) ++need;  // ceil(log2 n) + 2
-        if (lo_bits > 0 && hi_bits >= (need < 32 ? need : 32)) {
+        // and digit 4 must not be concentrated (a few distinct upper halves
+        // can vary in every bit): no bin above n / 32 (uniform keys: n / 256)
+        unsigned long long max4 = 0;
+        for (int b = 0; b < 256; ++b) max4 = ctr->spec4[b] > max4 ? ctr->spec4[b] : max4;
+        if (lo_bits > 0 && hi_bits >= (need < 32 ? need : 32) && !all_hist && max4 <= n / 32) {
             dmask = 0xF0u;
             plan->topfirst = 1;
         }

@@ -82,20 +82,32 @@ def test_ties_of_the_upper_half_are_ordered_by_the_fixup(ctx):
 
 
 def test_long_unsorted_runs_fall_back_to_the_full_sort(ctx):
+    """512 distinct upper halves (digit 4 looks spread out), random lower
+    halves: runs of ~8000 unsorted keys, so the fix-up raises its flag."""
     rng = np.random.default_rng(9)
-    tops = np.array([0x00000000, 0xFFFFFFFF, 0x5A5A5A5A, 0xA5A5A5A5], dtype=np.uint64)
-    hi = tops[rng.integers(0, 4, N)]
+    tops = rng.integers(0, 1 << 32, 512, dtype=np.uint64)
+    hi = tops[rng.integers(0, tops.size, N)]
     lo = rng.integers(0, 1 << 32, N, dtype=np.uint64)
     keys = (hi << np.uint64(32)) | lo
     check(ctx, keys, 4)  # the first sort's counters are the reported ones
+
+
+def test_few_distinct_upper_halves_take_the_plain_path(ctx):
+    """Four upper halves that differ in every bit: digit 4 is concentrated,
+    so the plan does not try the upper digits first."""
+    rng = np.random.default_rng(17)
+    tops = np.array([0x00000000, 0xFFFFFFFF, 0x5A5A5A5A, 0xA5A5A5A5], dtype=np.uint64)
+    hi = tops[rng.integers(0, 4, N)]
+    lo = rng.integers(0, 1 << 32, N, dtype=np.uint64)
+    check(ctx, (hi << np.uint64(32)) | lo, 8)
 
 
 def test_long_sorted_runs_fall_back(ctx):
     """Runs longer than the fix-up's scan window, already in order (equal
     keys): flagged, and the full sort keeps the payload stable."""
     rng = np.random.default_rng(10)
-    tops = rng.integers(0, 1 << 32, 64, dtype=np.uint64)
-    hi = tops[rng.integers(0, 64, N)]
+    tops = rng.integers(0, 1 << 32, 512, dtype=np.uint64)
+    hi = tops[rng.integers(0, tops.size, N)]
     keys = (hi << np.uint64(32)) | np.uint64(12345)
     check(ctx, keys, 4)
 
