@@ -86,6 +86,9 @@ constexpr int kRadix = 256;
 #ifndef B2S_U32_ITEMS
 #define B2S_U32_ITEMS 24
 #endif
+#ifndef B2S_U32_THREADS
+#define B2S_U32_THREADS 512
+#endif
 #ifndef B2S_U32_MINB
 #define B2S_U32_MINB 2  // CTAs per SM of that tile
 #endif
@@ -1947,7 +1950,7 @@ TileCfg tile_cfg(int kbytes, bool vals, uint64_t n) {
     if (kbytes == 4 && vals) return {512, 12, 2};
     // small sorts (the partitions of cfg1) are latency-bound: smaller tiles,
     // more CTAs (2^20 keys, p = 4: 0.088 vs 0.095 ms per partitioned sort)
-    if (kbytes == 4) return n < kTwinMinKeys ? TileCfg{512, 16, 2} : TileCfg{512, B2S_U32_ITEMS, B2S_U32_MINB};
+    if (kbytes == 4) return n < kTwinMinKeys ? TileCfg{512, 16, 2} : TileCfg{B2S_U32_THREADS, B2S_U32_ITEMS, B2S_U32_MINB};
     // 8-byte keys + payload: one 1024-thread CTA per SM with 8192-pair tiles
     // (per 2^28-pair pass 1.92 ms vs 1.97 for two 512-thread CTAs with
     // 4096-pair tiles)
@@ -1962,7 +1965,7 @@ b2s_status launch_passes(b2s_ctx* ctx, RadixPlan* plan, RadixCounters* ctr, uint
         return launch_passes_cfg<U, VALS, LB, 512, 12, 2>(ctx, plan, ctr, n, lb);
     } else if constexpr (sizeof(U) == 4) {
         if (c.items == 16) return launch_passes_cfg<U, VALS, LB, 512, 16, 2>(ctx, plan, ctr, n, lb);
-        return launch_passes_cfg<U, VALS, LB, 512, B2S_U32_ITEMS, B2S_U32_MINB>(ctx, plan, ctr, n, lb);
+        return launch_passes_cfg<U, VALS, LB, B2S_U32_THREADS, B2S_U32_ITEMS, B2S_U32_MINB>(ctx, plan, ctr, n, lb);
     } else if constexpr (VALS) {
         return launch_passes_cfg<U, VALS, LB, 1024, 8, 1>(ctx, plan, ctr, n, lb);
     } else {
