@@ -630,6 +630,9 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_LB_STEP
 #define B2S_LB_STEP 4
 #endif
+#ifndef B2S_LB_SKIP_EMPTY
+#define B2S_LB_SKIP_EMPTY 1
+#endif
 #ifndef B2S_TICKET_FIRST
 #define B2S_TICKET_FIRST 1  // keys-only first pass: offsets by fetch-and-add, no look-back
 #endif
@@ -837,7 +840,8 @@ struct TileShared {
 template <typename LB>
 __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, LB* __restrict__ lb_cur,
                                                                  const LB* lbw, uint32_t mycount,
-                                                                 unsigned long long lo) {
+                                                                 unsigned long long lo,
+                                                                 bool empty_digit = false) {
     using W = LookbackWord<LB>;
     constexpr int PRE = W::kPrefetch;
     constexpr int LOOKBACK = B2S_LB_STEP;
@@ -846,7 +850,9 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, 
     (void)lo;
     if (tile == 0) return 0;
     int64_t pred = (int64_t)tile - 1;
-    bool done = false;
+    // a digit no key of the pass has (its lane in every tile knows, from the
+    // pass's histogram) needs no prefix: its lanes sit the walk out
+    bool done = empty_digit;
     const LB* col = lb_cur + tid;
     LB* mine = lb_cur + (size_t)tile * kRadix + tid;
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1221,15 +1227,17 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
             // least dcount - (n - tile_base); the prefix is at most
             // min(tile_base, dcount), a window narrower than 2^30 (below)
             unsigned long long lo = 0;
+            bool empty_digit = false;
             if constexpr (sizeof(LB) == 4) {
                 const unsigned long long rest = sh.n - tile_base;
                 lo = sh.dcount[tid] > rest ? sh.dcount[tid] - rest : 0;
+                empty_digit = B2S_LB_SKIP_EMPTY && sh.dcount[tid] == 0;
             }
             // keys-only first pass: no order to keep among equal digits, so
             // a tile's offsets come from one fetch-and-add per digit in
             // arrival order -- no look-back chain
             const unsigned long long excl = ticket != nullptr ? atomicAdd(ticket + tid, (unsigned long long)mycount)
-                                                              : lookback_exclusive<LB>(tile, lb_cur, sh.lbw, mycount, lo);
+                                                              : lookback_exclusive<LB>(tile, lb_cur, sh.lbw, mycount, lo, empty_digit);
             gbase_out[tid] = (OFF)(sh.goff[tid] + excl - sh.start[tid]);
         }
     };
