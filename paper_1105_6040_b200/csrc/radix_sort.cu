@@ -630,6 +630,12 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_LB_STEP
 #define B2S_LB_STEP 4
 #endif
+// 32-bit look-back words: one lane walks two adjacent digits, reading and
+// publishing their two words as one 64-bit access (both always carry the same
+// flag), so four warps poll instead of eight.
+#ifndef B2S_LB_PAIR
+#define B2S_LB_PAIR 1
+#endif
 #ifndef B2S_LB_SKIP_EMPTY
 #define B2S_LB_SKIP_EMPTY 1
 #endif
@@ -897,6 +903,60 @@ __device__ __forceinline__ unsigned long long lookback_exclusive(uint32_t tile, 
     }
     if constexpr (sizeof(LB) == 4) excl = lo + ((excl - lo) & W::kMask);
     return excl;
+}
+
+// The same walk for a pair of adjacent digits (32-bit words): thread t < 128
+// owns digits 2t and 2t+1, whose words every tile publishes together in one
+// 64-bit store -- aggregates in the digit section, inclusive prefixes here --
+// so both carry the same flag and one 64-bit load serves both digits.
+__device__ __forceinline__ void lookback_exclusive_pair(uint32_t tile, uint32_t* __restrict__ lb_cur,
+                                                        uint32_t count0, uint32_t count1,
+                                                        unsigned long long lo0, unsigned long long lo1,
+                                                        bool empty_pair, unsigned long long& e0,
+                                                        unsigned long long& e1) {
+    using W = LookbackWord<uint32_t>;
+    constexpr int LOOKBACK = B2S_LB_STEP;
+    const int tid = threadIdx.x;
+    e0 = 0;
+    e1 = 0;
+    if (tile == 0) return;
+    int64_t pred = (int64_t)tile - 1;
+    bool done = empty_pair;
+    uint32_t x0 = 0, x1 = 0;  // prefixes modulo 2^30 (sums of 30-bit residues wrap in 32 bits harmlessly)
+    const unsigned long long* col = reinterpret_cast<const unsigned long long*>(lb_cur) + tid;
+    unsigned long long* mine = reinterpret_cast<unsigned long long*>(lb_cur) + (size_t)tile * (kRadix / 2) + tid;
+    auto publish = [&]() {
+        const uint32_t w0 = W::kInc | ((x0 + count0) & W::kMask), w1 = W::kInc | ((x1 + count1) & W::kMask);
+        st_relaxed(mine, (unsigned long long)w0 | ((unsigned long long)w1 << 32));
+    };
+    if (done) publish();
+    while (__any_sync(0xffffffffu, !done)) {
+        if (!done) {
+            unsigned long long w[LOOKBACK];
+#pragma unroll
+            for (int i = 0; i < LOOKBACK; ++i)
+                w[i] = (pred - i >= 0) ? ld_relaxed(col + (size_t)(pred - i) * (kRadix / 2))
+                                       : ((unsigned long long)W::kInc | ((unsigned long long)W::kInc << 32));
+            bool stop = false;
+#pragma unroll
+            for (int i = 0; i < LOOKBACK; ++i) {
+                const uint32_t a = (uint32_t)w[i], b = (uint32_t)(w[i] >> 32);
+                const uint32_t f = W::flag(a);  // == W::flag(b)
+                if (!stop && f != 0) {
+                    x0 += a & W::kMask;
+                    x1 += b & W::kMask;
+                    done = (f == 2);
+                    stop = done;
+                    pred -= done ? 0 : 1;
+                } else {
+                    stop = true;
+                }
+            }
+            if (done) publish();
+        }
+    }
+    e0 = lo0 + (((unsigned long long)x0 - lo0) & W::kMask);
+    e1 = lo1 + (((unsigned long long)x1 - lo1) & W::kMask);
 }
 
 // Per-warp early counts of one full tile: the warp's keys are counted into
@@ -1167,8 +1227,13 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
         if (ticket == nullptr) {
             LB* slot = lb_cur + (size_t)tile * kRadix + 2 * tid;
             const LB flag = tile == 0 ? W::kInc : W::kAgg;
-            st_relaxed(slot, flag | (LB)c0);
-            st_relaxed(slot + 1, flag | (LB)c1);
+            if constexpr (sizeof(LB) == 4 && B2S_LB_PAIR) {
+                st_relaxed(reinterpret_cast<unsigned long long*>(slot),
+                           (unsigned long long)(flag | (LB)c0) | ((unsigned long long)(flag | (LB)c1) << 32));
+            } else {
+                st_relaxed(slot, flag | (LB)c0);
+                st_relaxed(slot + 1, flag | (LB)c1);
+            }
         }
         uint32_t incl = c0 + c1;
 #pragma unroll
@@ -1220,6 +1285,24 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     // (independent loads) in a warp-uniform loop. Each lane publishes its
     // inclusive prefix the moment it is known.
     auto lookback = [&]() {
+        if constexpr (sizeof(LB) == 4 && B2S_LB_PAIR) {
+            if (ticket == nullptr) {
+                if (tid < kRadix / 2) {
+                    const uint32_t d0 = 2 * tid, d1 = 2 * tid + 1;
+                    const uint32_t s0 = sh.start[d0], s1 = sh.start[d1];
+                    const uint32_t s2 = d1 + 1 < kRadix ? sh.start[d1 + 1] : (uint32_t)tile_valid;
+                    const unsigned long long rest = sh.n - tile_base;
+                    const uint32_t h0 = sh.dcount[d0], h1 = sh.dcount[d1];
+                    unsigned long long e0, e1;
+                    lookback_exclusive_pair(tile, reinterpret_cast<uint32_t*>(lb_cur), s1 - s0, s2 - s1,
+                                            h0 > rest ? h0 - rest : 0, h1 > rest ? h1 - rest : 0,
+                                            B2S_LB_SKIP_EMPTY && h0 == 0 && h1 == 0, e0, e1);
+                    gbase_out[d0] = (OFF)(sh.goff[d0] + e0 - s0);
+                    gbase_out[d1] = (OFF)(sh.goff[d1] + e1 - s1);
+                }
+                return;
+            }
+        }
         if (tid < kRadix) {
             const uint32_t mycount = (tid + 1 < kRadix ? sh.start[tid + 1] : (uint32_t)tile_valid) - sh.start[tid];
             // 32-bit words: digit tid's keys in tiles >= tile number at most
