@@ -636,6 +636,13 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_LB_PAIR
 #define B2S_LB_PAIR 1
 #endif
+#ifndef B2S_LB_WARP0
+// first of the four paired look-back warps: not the four scanning warps
+// (0-3), which already carry the digit section (per 2^28 u32 pass, uniform /
+// ascending-but-one-pair: warp 0: 0.669 / 0.613 ms, 4: 0.667 / 0.599, 8 and
+// 12 the same as 4)
+#define B2S_LB_WARP0 4
+#endif
 #ifndef B2S_LB_SKIP_EMPTY
 #define B2S_LB_SKIP_EMPTY 1
 #endif
@@ -916,7 +923,7 @@ __device__ __forceinline__ void lookback_exclusive_pair(uint32_t tile, uint32_t*
                                                         unsigned long long& e1) {
     using W = LookbackWord<uint32_t>;
     constexpr int LOOKBACK = B2S_LB_STEP;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x - 32 * B2S_LB_WARP0;  // pair index
     e0 = 0;
     e1 = 0;
     if (tile == 0) return;
@@ -1287,8 +1294,9 @@ __device__ __forceinline__ void onesweep_tile(const Claim& claim_next, const Bet
     auto lookback = [&]() {
         if constexpr (sizeof(LB) == 4 && B2S_LB_PAIR) {
             if (ticket == nullptr) {
-                if (tid < kRadix / 2) {
-                    const uint32_t d0 = 2 * tid, d1 = 2 * tid + 1;
+                const int lt = tid - 32 * B2S_LB_WARP0;  // pair index of this thread
+                if (lt >= 0 && lt < kRadix / 2) {
+                    const uint32_t d0 = 2 * lt, d1 = 2 * lt + 1;
                     const uint32_t s0 = sh.start[d0], s1 = sh.start[d1];
                     const uint32_t s2 = d1 + 1 < kRadix ? sh.start[d1 + 1] : (uint32_t)tile_valid;
                     const unsigned long long rest = sh.n - tile_base;
