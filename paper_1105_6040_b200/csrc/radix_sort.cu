@@ -627,8 +627,11 @@ constexpr bool MATCH_SMEM = B2S_MATCH_HYBRID != 0;
 #ifndef B2S_ARITH_MIN_RANK
 #define B2S_ARITH_MIN_RANK 3  // 2 (regular kernel too): 0.750 vs 0.720 ms per 2^28 u32 pass
 #endif
+// predecessors read per look-back step. With the paired walk (two digits per
+// lane, 64-bit loads): 4: 0.667 ms per 2^28 u32 pass, 6: 0.664, 8: 0.667,
+// 12: 0.677 (cfg3 22.00 -> 21.95 ms with 6)
 #ifndef B2S_LB_STEP
-#define B2S_LB_STEP 4
+#define B2S_LB_STEP 6
 #endif
 // 32-bit look-back words: one lane walks two adjacent digits, reading and
 // publishing their two words as one 64-bit access (both always carry the same
